@@ -1,0 +1,214 @@
+/*
+ * kvx.h -- C ABI of the B200-native KVCache hot path (libkvx.so).
+ *
+ * Four stages of Mooncake's KVCache path (arXiv 2407.00079), each a
+ * hand-written sm_100a kernel or a copy-engine transfer:
+ *   1a  batched prefix block hash        kvx_chain_hash_batch
+ *   1b  batched prefix-match query       kvx_index_*, kvx_match_prefix_batch
+ *   2   gather paged -> contiguous       kvx_gather
+ *   3   layer-wise transfer              kvx_xfer_*, kvx_transfer_submit / _wait
+ *   4   scatter contiguous -> paged      kvx_scatter
+ *   2+3+4 fused paged -> paged           kvx_copy_paged (dst may be a peer view)
+ *
+ * Which reference interface each entry point replaces (reference =
+ * /root/reference, kvcsim; see INTEGRATION.md for the bindings):
+ *   kvx_chain_hash_batch   kvcsim::chain_hash            proj/include/kvcsim/kvcache.hpp:25
+ *                                                         (proj/src/kvcache.cpp:14-23)
+ *   kvx_index_insert       CachePool::admit_and_touch /  proj/include/kvcsim/kvcache.hpp:61-64
+ *                          insert_replicated (residency  proj/include/kvcsim/kvcache.hpp:68-69
+ *                          side of the block manager put)
+ *   kvx_index_erase        eviction in insert_block      proj/src/kvcache.cpp:72-97
+ *   kvx_index_lookup       CachePool::contains           proj/include/kvcsim/kvcache.hpp:74
+ *   kvx_match_prefix_batch CachePool::match_prefix,      proj/include/kvcsim/kvcache.hpp:72,105
+ *                          find_best_prefix_match        proj/include/kvcsim/conductor.hpp:63-64
+ *   kvx_gather / kvx_scatter / kvx_copy_paged / kvx_transfer_*:
+ *                          the analytic transfer model   proj/src/perf_model.cpp:51-59,
+ *                          and migration/stream events   proj/src/sim_engine.cpp:399-419,455-476,605-650
+ *                          (no byte-level reference exists)
+ *
+ * Conventions
+ *   - Every function returns kvx_status; on failure kvx_last_error() holds a
+ *     thread-local message.  KVX_EINVAL corresponds to kvcsim::ValidationError
+ *     (proj/include/kvcsim/errors.hpp:18-21).
+ *   - Pointers named d_* are device pointers on the device of the handle they
+ *     are used with; `stream` is a cudaStream_t passed as void* (NULL = the
+ *     legacy default stream).  Work is asynchronous and ordered on `stream`;
+ *     only *_wait, kvx_index_stats and kvx_sync are host-blocking.
+ *   - Calls on one handle must be externally serialised (the reference's
+ *     CachePool is single-owner, proj/include/kvcsim/kvcache.hpp:42-43).
+ *   - Block keys are int64.  Two values are reserved as table sentinels and
+ *     are never resident: KVX_KEY_EMPTY and KVX_KEY_TOMBSTONE.
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     entry point returns KVX_ECUDA.
+ */
+#ifndef KVX_H_
+#define KVX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVX_ABI_VERSION 1
+
+typedef enum {
+  KVX_OK = 0,
+  KVX_EINVAL = 1,    /* precondition violated (kvcsim::ValidationError) */
+  KVX_ENOMEM = 2,    /* device allocation failed */
+  KVX_ECUDA = 3,     /* CUDA runtime/driver error, or no device */
+  KVX_EABORTED = 4,  /* transfer source no longer resident (sim_engine.cpp:605-639) */
+  KVX_EAGAIN = 5     /* not complete yet (kvx_transfer_query) */
+} kvx_status;
+
+#define KVX_KEY_EMPTY ((int64_t)(-0x7FFFFFFFFFFFFFFFLL - 1))      /* INT64_MIN */
+#define KVX_KEY_TOMBSTONE ((int64_t)(-0x7FFFFFFFFFFFFFFFLL))      /* INT64_MIN + 1 */
+
+int kvx_abi_version(void);
+const char* kvx_last_error(void);
+/* Number of kernels this library has launched in this process. */
+uint64_t kvx_launch_count(void);
+/* Host-blocking stream synchronise (convenience for C hosts). */
+int kvx_sync(void* stream);
+
+/* ---- stage 1a: block hashing ------------------------------------------ */
+
+/* Scalar chain_hash (bit-identical to kvcsim::chain_hash, kvcache.cpp:14-23).
+ * Pure function, usable on hosts without a GPU. */
+int64_t kvx_chain_hash(int64_t prev_key, uint64_t content_hash);
+
+/* Batched prefix block keys.  Request r owns tokens [tok_off[r], tok_off[r+1])
+ * of d_tokens; its ceil(len/bs) keys go to d_keys[key_off[r] ...].
+ * content_i = fold(chain_hash, block tokens as uint32, from 0);
+ * key_i = chain_hash(key_{i-1}, content_i), key_{-1} = 0; the last block may
+ * be partial.  d_key_off must be the exclusive scan of ceil(len/bs). */
+int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req,
+                         int64_t bs, const int64_t* d_key_off, int64_t* d_keys, void* stream);
+
+/* ---- stage 1b: block index (GPU open-addressing table) + prefix match ---- */
+
+typedef struct kvx_index kvx_index;
+
+/* capacity_hint: expected resident keys; the table grows on demand. */
+int kvx_index_create(int device, int64_t capacity_hint, kvx_index** out);
+int kvx_index_destroy(kvx_index* idx);
+int kvx_index_device(const kvx_index* idx);
+/* Upsert keys (value = d_values[i], or the key's position i when NULL).
+ * Reserved sentinel keys are skipped and counted as rejected. */
+int kvx_index_insert(kvx_index* idx, const int64_t* d_keys, const int64_t* d_values, int64_t n,
+                     void* stream);
+int kvx_index_erase(kvx_index* idx, const int64_t* d_keys, int64_t n, void* stream);
+/* d_values_out[i] = value of key i, or -1 when absent. */
+int kvx_index_lookup(const kvx_index* idx, const int64_t* d_keys, int64_t n,
+                     int64_t* d_values_out, void* stream);
+int kvx_index_clear(kvx_index* idx, void* stream);
+/* Rebuild the table (drops tombstones) sized for at least min_keys keys. */
+int kvx_index_reserve(kvx_index* idx, int64_t min_keys, void* stream);
+/* Host-blocking: live keys, tombstones, slots, rejected sentinel keys. */
+int kvx_index_stats(kvx_index* idx, int64_t* live, int64_t* tombstones, int64_t* slots,
+                    int64_t* rejected, void* stream);
+
+/* Prefix match of n_req requests against n_inst instance indices (one
+ * kvcsim prefill instance each), all on the stream's device.
+ *   d_len_out[r*n_inst + i]  match_prefix of request r on instance i (optional)
+ *   d_best_len[r], d_best_id[r]  find_best_prefix_match: longest match, ties to
+ *                                the lowest inst_ids[i] (conductor.cpp:57-73)
+ * n_inst == 0 is KVX_EINVAL (the reference throws on an empty pool).
+ * inst_ids is a HOST array; n_inst <= KVX_MAX_INSTANCES. */
+#define KVX_MAX_INSTANCES 64
+int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+                           const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+                           int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
+                           void* stream);
+
+/* ---- paged KV pool ------------------------------------------------------ */
+
+/* HBM layout: base[((layer*2 + kv)*slots + slot) * slab], slab =
+ * block_size*heads*head_dim*dtype_bytes bytes (one block of one layer's K or
+ * V).  Transfer buffers for layers [lo,hi) and n blocks are laid out
+ * buf[(((l-lo)*2 + kv)*n + b) * slab]. */
+typedef struct {
+  int32_t layers;
+  int32_t block_size;
+  int32_t heads;
+  int32_t head_dim;
+  int32_t dtype_bytes;
+  int64_t slots;
+  int32_t device;
+} kvx_pool_desc;
+
+typedef struct kvx_pool kvx_pool;
+
+int kvx_pool_create(const kvx_pool_desc* desc, kvx_pool** out);
+/* Wrap memory the pool does not own (e.g. a peer pool mapped by kvx_ipc_open). */
+int kvx_pool_create_view(const kvx_pool_desc* desc, void* d_base, kvx_pool** out);
+int kvx_pool_destroy(kvx_pool* pool);
+void* kvx_pool_base(const kvx_pool* pool);
+int64_t kvx_pool_slab_bytes(const kvx_pool* pool);
+int64_t kvx_pool_bytes(const kvx_pool* pool);
+
+/* Synthetic content: 64-bit word w of slab (pool_id, layer, kv, slot) =
+ * mix64(slab_seed + w) (oracle/kvx_oracle.c). */
+int kvx_pool_fill_synthetic(kvx_pool* pool, uint32_t pool_id, void* stream);
+/* Counts 64-bit words of dst slabs (dst_table[b], layers [lo,hi)) that differ
+ * from the synthetic content of (src_pool_id, layer, kv, src_table[b]);
+ * atomically ADDS the count to *d_mismatch (uint64). */
+int kvx_pool_verify(const kvx_pool* dst, const int32_t* d_dst_table, uint32_t src_pool_id,
+                    const int32_t* d_src_table, int64_t n, int32_t layer_lo, int32_t layer_hi,
+                    uint64_t* d_mismatch, void* stream);
+
+/* ---- stages 2 / 4 / fused ------------------------------------------------ */
+
+int kvx_gather(const kvx_pool* pool, const int32_t* d_src_table, int64_t n, int32_t layer_lo,
+               int32_t layer_hi, void* d_buf, void* stream);
+int kvx_scatter(kvx_pool* pool, const int32_t* d_dst_table, int64_t n, int32_t layer_lo,
+                int32_t layer_hi, const void* d_buf, void* stream);
+/* dst[l][kv][dst_table[b]] = src[l][kv][src_table[b]].  dst may be a view of
+ * a peer GPU's pool (stores go over NVLink); src must be local to `stream`. */
+int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
+                   const int32_t* d_dst_table, int64_t n, int32_t layer_lo, int32_t layer_hi,
+                   void* stream);
+/* Copy-kernel variant selector (0 = LSU 128-bit, 1 = TMA bulk); default 0. */
+int kvx_set_copy_impl(int impl);
+
+/* ---- stage 3: transfer engine ----------------------------------------- */
+
+typedef struct kvx_xfer kvx_xfer;
+
+/* One in-order copy-engine queue per source device (the reference's
+ * per-sender FIFO, sim_engine.cpp:409-411). */
+int kvx_xfer_create(int device, kvx_xfer** out);
+int kvx_xfer_destroy(kvx_xfer* x);
+void* kvx_xfer_stream(kvx_xfer* x);
+/* Queue a copy of `bytes` from src to dst (either may be peer memory).  When
+ * after_stream is non-NULL the copy starts only after the work already queued
+ * on after_stream.  *ticket identifies the copy. */
+int kvx_transfer_submit(kvx_xfer* x, void* dst, const void* src, int64_t bytes,
+                        void* after_stream, uint64_t* ticket);
+/* Host-blocking wait for a ticket. */
+int kvx_transfer_wait(kvx_xfer* x, uint64_t ticket);
+/* Device-side wait: work queued on `stream` after this call runs after the copy. */
+int kvx_transfer_wait_stream(kvx_xfer* x, uint64_t ticket, void* stream);
+/* KVX_OK when complete, KVX_EAGAIN when still in flight. */
+int kvx_transfer_query(kvx_xfer* x, uint64_t ticket);
+/* Queue a 64-bit flag store of `value` to d_flag (local or peer) on the
+ * transfer queue, ordered after every copy submitted before it. */
+int kvx_transfer_signal(kvx_xfer* x, void* d_flag, uint64_t value);
+
+/* ---- cross-process plumbing (one process per GPU) ---------------------- */
+
+#define KVX_IPC_HANDLE_BYTES 64
+int kvx_ipc_export(void* d_ptr, uint8_t handle[KVX_IPC_HANDLE_BYTES]);
+int kvx_ipc_open(const uint8_t handle[KVX_IPC_HANDLE_BYTES], int device, void** d_ptr);
+int kvx_ipc_close(void* d_ptr);
+int kvx_enable_peer(int device, int peer_device);
+/* Stream-ordered flag store / wait (no kernel spins: the stream front end
+ * waits).  wait: proceeds once *(uint64*)d_flag >= value. */
+int kvx_signal_write(void* stream, void* d_flag, uint64_t value);
+int kvx_signal_wait(void* stream, const void* d_flag, uint64_t value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVX_H_ */

@@ -1,0 +1,465 @@
+// kvx_copy.cu -- paged KV pools and the byte stages: K3 gather (stage 2),
+// K5 scatter (stage 4) and the fused paged -> paged copy (stages 2+3+4, whose
+// destination may be a peer GPU's pool mapped over NVLink).
+//
+// There is no byte-level reference.  What moves is defined
+// by the reference's block selection: the whole hash_ids chain of a request
+// for the prefill -> decode stream (proj/src/sim_engine.cpp:463-464), a chain
+// range [local_prefix, used_prefix) for a migration
+// (proj/src/sim_engine.cpp:405-416), landing positions per insert_replicated
+// (proj/src/kvcache.cpp:133-148).  Sizes follow kv_bytes_per_token
+// (proj/src/config.cpp:216).
+//
+// Every stage is one generic slab copy: unit u = (plane, b) with plane =
+// (layer - lo)*2 + kv; the source / destination address of a unit is either
+// a paged slot (table[b]) or a contiguous buffer position (b).  Two
+// implementations, both HBM-bound (no tensor-core work exists here):
+//   LSU  -- 512-thread CTAs, each CTA streams whole work items of up to
+//           32 KiB: all 128-bit loads (ld.global.nc.L1::no_allocate) are
+//           issued before any store, 4 per thread in flight.
+//   TMA  -- one elected thread per CTA drives cp.async.bulk global->shared
+//           (mbarrier complete_tx) and shared->global bulk stores through an
+//           8-stage shared-memory ring: 4 loads and up to 4 stores in flight
+//           per SM with no register staging.
+#include <algorithm>
+
+#include "kvx_common.cuh"
+
+namespace kvx {
+namespace {
+
+int g_copy_impl = 0;
+
+struct SlabCopy {
+  const uint8_t* src;
+  uint8_t* dst;
+  int64_t src_plane;  // bytes between (layer, kv) planes on the source side
+  int64_t dst_plane;
+  const int32_t* src_table;  // NULL: contiguous side
+  const int32_t* dst_table;
+  int64_t n;       // blocks per plane
+  int64_t planes;  // (hi - lo) * 2
+  int64_t slab;    // bytes per unit, multiple of 16
+};
+
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void unit_addrs(const SlabCopy& c, int64_t u, const uint8_t*& s,
+                                           uint8_t*& d) {
+  const int64_t plane = u / c.n;
+  const int64_t b = u - plane * c.n;
+  const int64_t sb = c.src_table ? static_cast<int64_t>(__ldg(c.src_table + b)) : b;
+  const int64_t db = c.dst_table ? static_cast<int64_t>(__ldg(c.dst_table + b)) : b;
+  s = c.src + plane * c.src_plane + sb * c.slab;
+  d = c.dst + plane * c.dst_plane + db * c.slab;
+}
+
+constexpr int kLsuThreads = 512;
+constexpr int kLsuUnroll = 4;
+constexpr int64_t kLsuItem = 16LL * kLsuThreads * kLsuUnroll;  // 32 KiB
+
+__global__ void __launch_bounds__(kLsuThreads) copy_lsu_kernel(const SlabCopy c) {
+  const int64_t parts = (c.slab + kLsuItem - 1) / kLsuItem;
+  const int64_t items = c.planes * c.n * parts;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t u = it / parts;
+    const int64_t off = (it - u * parts) * kLsuItem;
+    const uint8_t* s;
+    uint8_t* d;
+    unit_addrs(c, u, s, d);
+    const int64_t bytes = min(kLsuItem, c.slab - off);
+    const int4* sv = reinterpret_cast<const int4*>(s + off);
+    int4* dv = reinterpret_cast<int4*>(d + off);
+    const int nv = static_cast<int>(bytes >> 4);
+    int4 r[kLsuUnroll];
+#pragma unroll
+    for (int j = 0; j < kLsuUnroll; ++j) {
+      const int v = threadIdx.x + j * kLsuThreads;
+      if (v < nv) r[j] = ld_stream(sv + v);
+    }
+#pragma unroll
+    for (int j = 0; j < kLsuUnroll; ++j) {
+      const int v = threadIdx.x + j * kLsuThreads;
+      if (v < nv) dv[v] = r[j];
+    }
+  }
+}
+
+// ---- TMA bulk-copy pipeline ----------------------------------------------
+constexpr int kTmaStages = 8;
+constexpr int kTmaAhead = 4;                 // loads in flight
+constexpr int64_t kTmaStage = 16 * 1024;     // bytes per stage
+constexpr int kTmaSmem = kTmaStages * kTmaStage;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* smem, const void* gsrc, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(32) copy_tma_kernel(const SlabCopy c) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+  const int64_t parts = (c.slab + kTmaStage - 1) / kTmaStage;
+  const int64_t items = c.planes * c.n * parts;
+  // this CTA's items: blockIdx.x, blockIdx.x + gridDim.x, ...
+  const int64_t mine = items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  auto item_addr = [&](int64_t k, const uint8_t*& s, uint8_t*& d, uint32_t& bytes) {
+    const int64_t it = blockIdx.x + k * gridDim.x;
+    const int64_t u = it / parts;
+    const int64_t off = (it - u * parts) * kTmaStage;
+    unit_addrs(c, u, s, d);
+    s += off;
+    d += off;
+    bytes = static_cast<uint32_t>(min(kTmaStage, c.slab - off));
+  };
+
+  for (int64_t k = 0; k < mine + kTmaAhead; ++k) {
+    // consume item k - kTmaAhead: its load has landed -> bulk store it out
+    const int64_t kc = k - kTmaAhead;
+    if (kc >= 0) {
+      const int st = static_cast<int>(kc % kTmaStages);
+      mbar_wait(&bars[st], static_cast<uint32_t>((kc / kTmaStages) & 1));
+      const uint8_t* s;
+      uint8_t* d;
+      uint32_t bytes;
+      item_addr(kc, s, d, bytes);
+      bulk_store(d, smem + st * kTmaStage, bytes);
+    }
+    // produce item k into its stage once the store that last used it has
+    // finished reading shared memory (stores committed: items <= kc; the
+    // stage's previous user is item k - kTmaStages).
+    if (k < mine) {
+      if (k >= kTmaStages) bulk_wait_read<kTmaStages - kTmaAhead>();
+      const int st = static_cast<int>(k % kTmaStages);
+      const uint8_t* s;
+      uint8_t* d;
+      uint32_t bytes;
+      item_addr(k, s, d, bytes);
+      mbar_expect_tx(&bars[st], bytes);
+      bulk_load(smem + st * kTmaStage, s, bytes, &bars[st]);
+    }
+  }
+  bulk_wait_all();
+}
+
+int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
+  const int64_t units = c.planes * c.n;
+  if (units == 0 || c.slab == 0) return KVX_OK;
+  const int sms = sm_count(dev);
+  if (g_copy_impl == 1) {
+    static bool attr_set[64] = {false};
+    if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+      KVX_CUDA(cudaFuncSetAttribute(copy_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kTmaSmem));
+      attr_set[dev] = true;
+    }
+    const int64_t items = units * ((c.slab + kTmaStage - 1) / kTmaStage);
+    const int blocks = static_cast<int>(std::min<int64_t>(items, static_cast<int64_t>(sms)));
+    copy_tma_kernel<<<blocks, 32, kTmaSmem, s>>>(c);
+    KVX_LAUNCH_CHECK("copy_tma_kernel");
+  } else {
+    const int64_t items = units * ((c.slab + kLsuItem - 1) / kLsuItem);
+    const int blocks =
+        static_cast<int>(std::min<int64_t>(items, static_cast<int64_t>(sms) * 4));
+    copy_lsu_kernel<<<blocks, kLsuThreads, 0, s>>>(c);
+    KVX_LAUNCH_CHECK("copy_lsu_kernel");
+  }
+  return KVX_OK;
+}
+
+// ---- synthetic content ------------------------------------------------------
+
+__global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ base, uint32_t pool_id,
+                                                   int64_t slots, int64_t units, int64_t slab) {
+  const int64_t words = slab >> 3;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t lk = u / slots;
+    const int64_t slot = u - lk * slots;
+    const uint64_t seed = slab_seed(pool_id, static_cast<uint32_t>(lk >> 1),
+                                    static_cast<uint32_t>(lk & 1), static_cast<uint32_t>(slot));
+    ulonglong2* p = reinterpret_cast<ulonglong2*>(base + u * slab);
+    for (int64_t v = threadIdx.x; v < (words >> 1); v += blockDim.x) {
+      ulonglong2 w;
+      w.x = mix64(seed + 2 * v);
+      w.y = mix64(seed + 2 * v + 1);
+      p[v] = w;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) verify_kernel(const uint8_t* __restrict__ base,
+                                                     int64_t slots, int64_t slab,
+                                                     const int32_t* __restrict__ dst_table,
+                                                     uint32_t src_pool_id,
+                                                     const int32_t* __restrict__ src_table,
+                                                     int64_t n, int32_t layer_lo, int64_t planes,
+                                                     unsigned long long* __restrict__ mismatch) {
+  const int64_t words = slab >> 3;
+  unsigned long long bad = 0;
+  for (int64_t u = blockIdx.x; u < planes * n; u += gridDim.x) {
+    const int64_t plane = u / n;
+    const int64_t b = u - plane * n;
+    const int64_t layer = layer_lo + (plane >> 1);
+    const int kv = static_cast<int>(plane & 1);
+    const uint64_t seed = slab_seed(src_pool_id, static_cast<uint32_t>(layer),
+                                    static_cast<uint32_t>(kv),
+                                    static_cast<uint32_t>(src_table[b]));
+    const ulonglong2* p = reinterpret_cast<const ulonglong2*>(
+        base + ((layer * 2 + kv) * slots + dst_table[b]) * slab);
+    for (int64_t v = threadIdx.x; v < (words >> 1); v += blockDim.x) {
+      const ulonglong2 w = p[v];
+      bad += (w.x != mix64(seed + 2 * v)) + (w.y != mix64(seed + 2 * v + 1));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatch, bad);
+}
+
+}  // namespace
+}  // namespace kvx
+
+using namespace kvx;
+
+struct kvx_pool {
+  kvx_pool_desc d;
+  int64_t slab = 0;
+  int64_t bytes = 0;
+  uint8_t* base = nullptr;
+  bool owned = false;
+};
+
+namespace {
+
+int check_desc(const kvx_pool_desc* d) {
+  KVX_REQUIRE(d != nullptr, "kvx_pool: NULL descriptor");
+  KVX_REQUIRE(d->layers >= 1 && d->layers <= 32767, "kvx_pool: layers must be in [1, 32767]");
+  KVX_REQUIRE(d->block_size >= 1 && d->heads >= 1 && d->head_dim >= 1,
+              "kvx_pool: block_size, heads, head_dim must be >= 1");
+  KVX_REQUIRE(d->dtype_bytes == 1 || d->dtype_bytes == 2 || d->dtype_bytes == 4,
+              "kvx_pool: dtype_bytes must be 1, 2 or 4");
+  KVX_REQUIRE(d->slots >= 1 && d->slots <= 0x7FFFFFFF, "kvx_pool: slots must be in [1, 2^31)");
+  const int64_t slab = static_cast<int64_t>(d->block_size) * d->heads * d->head_dim * d->dtype_bytes;
+  KVX_REQUIRE(slab % 16 == 0, "kvx_pool: slab bytes must be a multiple of 16");
+  return KVX_OK;
+}
+
+int check_range(const kvx_pool* p, int64_t n, int32_t lo, int32_t hi) {
+  KVX_REQUIRE(p != nullptr, "NULL pool");
+  KVX_REQUIRE(n >= 0, "block count must be >= 0");
+  KVX_REQUIRE(lo >= 0 && lo <= hi && hi <= p->d.layers, "bad layer range");
+  return KVX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kvx_pool_create(const kvx_pool_desc* desc, kvx_pool** out) {
+  int st = check_desc(desc);
+  if (st) return st;
+  KVX_REQUIRE(out != nullptr, "kvx_pool_create: out is NULL");
+  DeviceGuard g(desc->device);
+  auto* p = new kvx_pool();
+  p->d = *desc;
+  p->slab = static_cast<int64_t>(desc->block_size) * desc->heads * desc->head_dim * desc->dtype_bytes;
+  p->bytes = static_cast<int64_t>(desc->layers) * 2 * desc->slots * p->slab;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->base), static_cast<size_t>(p->bytes));
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_error(e, "kvx_pool_create: cudaMalloc");
+  }
+  p->owned = true;
+  *out = p;
+  return KVX_OK;
+}
+
+int kvx_pool_create_view(const kvx_pool_desc* desc, void* d_base, kvx_pool** out) {
+  int st = check_desc(desc);
+  if (st) return st;
+  KVX_REQUIRE(out != nullptr && d_base != nullptr, "kvx_pool_create_view: NULL");
+  KVX_REQUIRE((reinterpret_cast<uintptr_t>(d_base) & 15) == 0,
+              "kvx_pool_create_view: base must be 16-byte aligned");
+  auto* p = new kvx_pool();
+  p->d = *desc;
+  p->slab = static_cast<int64_t>(desc->block_size) * desc->heads * desc->head_dim * desc->dtype_bytes;
+  p->bytes = static_cast<int64_t>(desc->layers) * 2 * desc->slots * p->slab;
+  p->base = static_cast<uint8_t*>(d_base);
+  p->owned = false;
+  *out = p;
+  return KVX_OK;
+}
+
+int kvx_pool_destroy(kvx_pool* p) {
+  if (!p) return KVX_OK;
+  if (p->owned && p->base) {
+    DeviceGuard g(p->d.device);
+    cudaFree(p->base);
+  }
+  delete p;
+  return KVX_OK;
+}
+
+void* kvx_pool_base(const kvx_pool* p) { return p ? p->base : nullptr; }
+int64_t kvx_pool_slab_bytes(const kvx_pool* p) { return p ? p->slab : 0; }
+int64_t kvx_pool_bytes(const kvx_pool* p) { return p ? p->bytes : 0; }
+
+int kvx_set_copy_impl(int impl) {
+  KVX_REQUIRE(impl == 0 || impl == 1, "kvx_set_copy_impl: impl must be 0 (LSU) or 1 (TMA)");
+  g_copy_impl = impl;
+  return KVX_OK;
+}
+
+int kvx_pool_fill_synthetic(kvx_pool* p, uint32_t pool_id, void* stream) {
+  KVX_REQUIRE(p != nullptr, "kvx_pool_fill_synthetic: NULL pool");
+  DeviceGuard g(p->d.device);
+  const int64_t units = static_cast<int64_t>(p->d.layers) * 2 * p->d.slots;
+  const int blocks = static_cast<int>(std::min<int64_t>(units, sm_count(p->d.device) * 8));
+  fill_kernel<<<blocks, 256, 0, as_stream(stream)>>>(p->base, pool_id, p->d.slots, units, p->slab);
+  KVX_LAUNCH_CHECK("fill_kernel");
+  return KVX_OK;
+}
+
+int kvx_pool_verify(const kvx_pool* dst, const int32_t* d_dst_table, uint32_t src_pool_id,
+                    const int32_t* d_src_table, int64_t n, int32_t layer_lo, int32_t layer_hi,
+                    uint64_t* d_mismatch, void* stream) {
+  int st = check_range(dst, n, layer_lo, layer_hi);
+  if (st) return st;
+  KVX_REQUIRE(d_mismatch != nullptr, "kvx_pool_verify: NULL counter");
+  if (n == 0 || layer_hi == layer_lo) return KVX_OK;
+  KVX_REQUIRE(d_dst_table && d_src_table, "kvx_pool_verify: NULL table");
+  DeviceGuard g(dst->d.device);
+  const int64_t planes = static_cast<int64_t>(layer_hi - layer_lo) * 2;
+  const int blocks =
+      static_cast<int>(std::min<int64_t>(planes * n, sm_count(dst->d.device) * 8));
+  verify_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      dst->base, dst->d.slots, dst->slab, d_dst_table, src_pool_id, d_src_table, n, layer_lo,
+      planes, reinterpret_cast<unsigned long long*>(d_mismatch));
+  KVX_LAUNCH_CHECK("verify_kernel");
+  return KVX_OK;
+}
+
+int kvx_gather(const kvx_pool* p, const int32_t* d_src_table, int64_t n, int32_t lo, int32_t hi,
+               void* d_buf, void* stream) {
+  int st = check_range(p, n, lo, hi);
+  if (st) return st;
+  if (n == 0 || lo == hi) return KVX_OK;
+  KVX_REQUIRE(d_src_table && d_buf, "kvx_gather: NULL table or buffer");
+  KVX_REQUIRE((reinterpret_cast<uintptr_t>(d_buf) & 15) == 0, "kvx_gather: buffer not 16B aligned");
+  SlabCopy c;
+  c.src = p->base + static_cast<int64_t>(lo) * 2 * p->d.slots * p->slab;
+  c.src_plane = p->d.slots * p->slab;
+  c.src_table = d_src_table;
+  c.dst = static_cast<uint8_t*>(d_buf);
+  c.dst_plane = n * p->slab;
+  c.dst_table = nullptr;
+  c.n = n;
+  c.planes = static_cast<int64_t>(hi - lo) * 2;
+  c.slab = p->slab;
+  DeviceGuard g(p->d.device);
+  return launch_copy(c, p->d.device, as_stream(stream));
+}
+
+int kvx_scatter(kvx_pool* p, const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi,
+                const void* d_buf, void* stream) {
+  int st = check_range(p, n, lo, hi);
+  if (st) return st;
+  if (n == 0 || lo == hi) return KVX_OK;
+  KVX_REQUIRE(d_dst_table && d_buf, "kvx_scatter: NULL table or buffer");
+  KVX_REQUIRE((reinterpret_cast<uintptr_t>(d_buf) & 15) == 0,
+              "kvx_scatter: buffer not 16B aligned");
+  SlabCopy c;
+  c.src = static_cast<const uint8_t*>(d_buf);
+  c.src_plane = n * p->slab;
+  c.src_table = nullptr;
+  c.dst = p->base + static_cast<int64_t>(lo) * 2 * p->d.slots * p->slab;
+  c.dst_plane = p->d.slots * p->slab;
+  c.dst_table = d_dst_table;
+  c.n = n;
+  c.planes = static_cast<int64_t>(hi - lo) * 2;
+  c.slab = p->slab;
+  DeviceGuard g(p->d.device);
+  return launch_copy(c, p->d.device, as_stream(stream));
+}
+
+int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
+                   const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, void* stream) {
+  int st = check_range(src, n, lo, hi);
+  if (st) return st;
+  st = check_range(dst, n, lo, hi);
+  if (st) return st;
+  KVX_REQUIRE(src->slab == dst->slab, "kvx_copy_paged: slab sizes differ");
+  if (n == 0 || lo == hi) return KVX_OK;
+  KVX_REQUIRE(d_src_table && d_dst_table, "kvx_copy_paged: NULL table");
+  SlabCopy c;
+  c.src = src->base + static_cast<int64_t>(lo) * 2 * src->d.slots * src->slab;
+  c.src_plane = src->d.slots * src->slab;
+  c.src_table = d_src_table;
+  c.dst = dst->base + static_cast<int64_t>(lo) * 2 * dst->d.slots * dst->slab;
+  c.dst_plane = dst->d.slots * dst->slab;
+  c.dst_table = d_dst_table;
+  c.n = n;
+  c.planes = static_cast<int64_t>(hi - lo) * 2;
+  c.slab = src->slab;
+  DeviceGuard g(src->d.device);
+  return launch_copy(c, src->d.device, as_stream(stream));
+}
+
+}  // extern "C"

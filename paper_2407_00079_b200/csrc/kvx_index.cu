@@ -1,0 +1,544 @@
+// kvx_index.cu -- the block index (residency side of the block manager) and
+// K2, the batched prefix-match query (stage 1b).
+//
+// Reference semantics:
+//   residency      CachePool::contains / resident_ map  (proj/include/kvcsim/kvcache.hpp:74,98)
+//   match_prefix   largest k with blocks[0..k) resident, stops at the FIRST
+//                  miss even if later blocks are resident (proj/src/kvcache.cpp:150-154)
+//   best match     max over instances; ties -> lowest instance id; first
+//                  instance seeds (proj/src/conductor.cpp:57-73)
+//
+// Table: open addressing, linear probing, power-of-two slots, structure of
+// arrays (keys[] and values[] separate) so a match probe touches only the
+// 8-byte key array -- 4 keys per 32-byte sector.  Slot = mix64(key) & mask.
+// Erase writes a tombstone; tombstones are dropped by a rebuild that the host
+// triggers from an upper bound on occupied slots (no per-call sync).
+//
+// Match mapping: one warp per (request, instance) task.  Each lane probes two
+// query keys per iteration (64 keys per warp step, two independent probe
+// chains per lane in flight); __ballot_sync over "miss" and __ffs give the
+// first miss, so the warp exits at the first window containing a miss.  The
+// per-request argmax over instances is one atomicMax per task on a packed
+// (len << 32 | ~id) word, which reproduces the lowest-id tie-break.
+#include <algorithm>
+
+#include "kvx_common.cuh"
+
+namespace kvx {
+namespace {
+
+constexpr double kMaxLoad = 0.70;     // occupied (live + tombstones) / slots
+constexpr double kTargetLoad = 0.40;  // after a rebuild
+
+struct Counters {
+  unsigned long long live;
+  unsigned long long used;      // live + tombstones
+  unsigned long long rejected;  // reserved sentinel keys seen by insert
+};
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void fill_i64(int64_t* __restrict__ p, int64_t n, int64_t v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+__device__ __forceinline__ void insert_one(int64_t* __restrict__ tkeys,
+                                           int64_t* __restrict__ tvals, uint64_t mask,
+                                           int64_t key, int64_t val, unsigned long long& added) {
+  uint64_t s = mix64(static_cast<uint64_t>(key)) & mask;
+  while (true) {
+    int64_t cur = tkeys[s];
+    if (cur == key) {
+      tvals[s] = val;
+      return;
+    }
+    if (cur == kKeyEmpty) {
+      const int64_t prev = static_cast<int64_t>(atomicCAS(
+          reinterpret_cast<unsigned long long*>(tkeys + s),
+          static_cast<unsigned long long>(kKeyEmpty), static_cast<unsigned long long>(key)));
+      if (prev == kKeyEmpty) {
+        tvals[s] = val;
+        ++added;
+        return;
+      }
+      if (prev == key) {
+        tvals[s] = val;
+        return;
+      }
+    }
+    s = (s + 1) & mask;
+  }
+}
+
+__global__ void __launch_bounds__(256) insert_kernel(int64_t* __restrict__ tkeys,
+                                                     int64_t* __restrict__ tvals, uint64_t mask,
+                                                     const int64_t* __restrict__ keys,
+                                                     const int64_t* __restrict__ vals, int64_t n,
+                                                     Counters* __restrict__ ctr) {
+  unsigned long long added = 0, rejected = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t key = keys[i];
+    if (is_reserved(key)) {
+      ++rejected;
+      continue;
+    }
+    insert_one(tkeys, tvals, mask, key, vals ? vals[i] : i, added);
+  }
+  added = warp_sum(added);
+  rejected = warp_sum(rejected);
+  if ((threadIdx.x & 31) == 0) {
+    if (added) {
+      atomicAdd(&ctr->live, added);
+      atomicAdd(&ctr->used, added);
+    }
+    if (rejected) atomicAdd(&ctr->rejected, rejected);
+  }
+}
+
+__global__ void __launch_bounds__(256) erase_kernel(int64_t* __restrict__ tkeys, uint64_t mask,
+                                                    const int64_t* __restrict__ keys, int64_t n,
+                                                    Counters* __restrict__ ctr) {
+  unsigned long long removed = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t key = keys[i];
+    if (is_reserved(key)) continue;
+    uint64_t s = mix64(static_cast<uint64_t>(key)) & mask;
+    while (true) {
+      const int64_t cur = tkeys[s];
+      if (cur == kKeyEmpty) break;
+      if (cur == key) {
+        const int64_t prev = static_cast<int64_t>(
+            atomicCAS(reinterpret_cast<unsigned long long*>(tkeys + s),
+                      static_cast<unsigned long long>(key),
+                      static_cast<unsigned long long>(kKeyTomb)));
+        if (prev == key) ++removed;
+        break;
+      }
+      s = (s + 1) & mask;
+    }
+  }
+  removed = warp_sum(removed);
+  if ((threadIdx.x & 31) == 0 && removed)
+    atomicAdd(&ctr->live, static_cast<unsigned long long>(-static_cast<long long>(removed)));
+}
+
+__device__ __forceinline__ int64_t find_slot(const int64_t* __restrict__ tkeys, uint64_t mask,
+                                             int64_t key) {
+  if (is_reserved(key)) return -1;
+  uint64_t s = mix64(static_cast<uint64_t>(key)) & mask;
+  while (true) {
+    const int64_t cur = __ldg(tkeys + s);
+    if (cur == key) return static_cast<int64_t>(s);
+    if (cur == kKeyEmpty) return -1;
+    s = (s + 1) & mask;
+  }
+}
+
+__global__ void __launch_bounds__(256) lookup_kernel(const int64_t* __restrict__ tkeys,
+                                                     const int64_t* __restrict__ tvals,
+                                                     uint64_t mask,
+                                                     const int64_t* __restrict__ keys, int64_t n,
+                                                     int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = find_slot(tkeys, mask, keys[i]);
+    out[i] = s < 0 ? -1 : tvals[s];
+  }
+}
+
+__global__ void __launch_bounds__(256) rehash_kernel(const int64_t* __restrict__ okeys,
+                                                     const int64_t* __restrict__ ovals,
+                                                     int64_t oslots, int64_t* __restrict__ nkeys,
+                                                     int64_t* __restrict__ nvals, uint64_t nmask,
+                                                     Counters* __restrict__ ctr) {
+  unsigned long long added = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < oslots;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t key = okeys[i];
+    if (is_reserved(key)) continue;
+    insert_one(nkeys, nvals, nmask, key, ovals[i], added);
+  }
+  added = warp_sum(added);
+  if ((threadIdx.x & 31) == 0 && added) {
+    atomicAdd(&ctr->live, added);
+    atomicAdd(&ctr->used, added);
+  }
+}
+
+// ---- K2: batched prefix match ------------------------------------------
+
+struct MatchParams {
+  const int64_t* keys[KVX_MAX_INSTANCES];
+  uint64_t mask[KVX_MAX_INSTANCES];
+  int32_t ids[KVX_MAX_INSTANCES];
+  int32_t n_inst;
+};
+
+// Two independent probe chains per lane: issue both first loads before
+// resolving either, so each lane keeps two random L2/HBM reads in flight.
+__device__ __forceinline__ void probe2(const int64_t* __restrict__ tk, uint64_t mask,
+                                       int64_t k0, bool v0, int64_t k1, bool v1, bool& h0,
+                                       bool& h1) {
+  bool d0 = !v0 || is_reserved(k0), d1 = !v1 || is_reserved(k1);
+  h0 = false;
+  h1 = false;
+  uint64_t s0 = mix64(static_cast<uint64_t>(k0)) & mask;
+  uint64_t s1 = mix64(static_cast<uint64_t>(k1)) & mask;
+  while (!(d0 && d1)) {
+    const int64_t c0 = d0 ? kKeyEmpty : __ldg(tk + s0);
+    const int64_t c1 = d1 ? kKeyEmpty : __ldg(tk + s1);
+    if (!d0) {
+      if (c0 == k0) {
+        h0 = true;
+        d0 = true;
+      } else if (c0 == kKeyEmpty) {
+        d0 = true;
+      } else {
+        s0 = (s0 + 1) & mask;
+      }
+    }
+    if (!d1) {
+      if (c1 == k1) {
+        h1 = true;
+        d1 = true;
+      } else if (c1 == kKeyEmpty) {
+        d1 = true;
+      } else {
+        s1 = (s1 + 1) & mask;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long pack_best(int64_t len, int32_t id) {
+  // Larger len wins; on equal len the LOWER id must win, so store ~ordered(id).
+  const uint32_t ordered = static_cast<uint32_t>(id) ^ 0x80000000u;
+  return (static_cast<unsigned long long>(len) << 32) | static_cast<unsigned long long>(~ordered);
+}
+
+__global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ MatchParams p,
+                                                    const int64_t* __restrict__ keys,
+                                                    const int64_t* __restrict__ key_off,
+                                                    int64_t n_req,
+                                                    int64_t* __restrict__ len_out,
+                                                    int64_t* __restrict__ best_len,
+                                                    int32_t* __restrict__ best_id) {
+  const int lane = threadIdx.x & 31;
+  const int64_t tasks = n_req * p.n_inst;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       t < tasks; t += warps) {
+    const int64_t r = t / p.n_inst;
+    const int i = static_cast<int>(t - r * p.n_inst);
+    const int64_t* __restrict__ tk = p.keys[i];
+    const uint64_t mask = p.mask[i];
+    const int64_t base = key_off[r];
+    const int64_t n = key_off[r + 1] - base;
+    const int64_t* __restrict__ q = keys + base;
+    int64_t len = 0;
+    for (int64_t k0 = 0;; k0 += 64) {
+      const int64_t j0 = k0 + lane, j1 = k0 + 32 + lane;
+      const bool v0 = j0 < n, v1 = j1 < n;
+      const int64_t q0 = v0 ? __ldg(q + j0) : 0;
+      const int64_t q1 = v1 ? __ldg(q + j1) : 0;
+      bool h0, h1;
+      probe2(tk, mask, q0, v0, q1, v1, h0, h1);
+      const unsigned m0 = __ballot_sync(0xffffffffu, !h0);
+      const unsigned m1 = __ballot_sync(0xffffffffu, !h1);
+      if (m0) {
+        len = k0 + __ffs(m0) - 1;
+        break;
+      }
+      if (m1) {
+        len = k0 + 32 + __ffs(m1) - 1;
+        break;
+      }
+    }
+    if (lane == 0) {
+      if (len_out) len_out[t] = len;
+      if (best_len) {
+        if (p.n_inst == 1) {
+          best_len[r] = len;
+          best_id[r] = p.ids[0];
+        } else {
+          atomicMax(reinterpret_cast<unsigned long long*>(best_len + r), pack_best(len, p.ids[i]));
+        }
+      }
+    }
+  }
+}
+
+__global__ void unpack_best_kernel(int64_t* __restrict__ best_len, int32_t* __restrict__ best_id,
+                                   int64_t n_req) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_req;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long v = static_cast<unsigned long long>(best_len[r]);
+    best_len[r] = static_cast<int64_t>(v >> 32);
+    best_id[r] = static_cast<int32_t>(~static_cast<uint32_t>(v & 0xffffffffu) ^ 0x80000000u);
+  }
+}
+
+int grid_for(int64_t n, int threads, int dev, int per_sm = 8) {
+  const int64_t want = (n + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(sm_count(dev)) * per_sm;
+  return static_cast<int>(std::max<int64_t>(1, std::min(want, cap)));
+}
+
+int64_t next_pow2(int64_t v) {
+  int64_t p = 1024;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace
+}  // namespace kvx
+
+using namespace kvx;
+
+struct kvx_index {
+  int device = 0;
+  int64_t* keys = nullptr;
+  int64_t* vals = nullptr;
+  int64_t slots = 0;
+  Counters* ctr = nullptr;   // device counters
+  int64_t used_ub = 0;       // host upper bound on occupied slots
+};
+
+namespace {
+
+int alloc_table(kvx_index* x, int64_t slots, cudaStream_t s, int64_t** keys, int64_t** vals) {
+  KVX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(keys), sizeof(int64_t) * slots, s));
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(vals), sizeof(int64_t) * slots, s);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(*keys, s);
+    return cuda_error(e, "kvx_index: cudaMallocAsync(values)");
+  }
+  fill_i64<<<grid_for(slots, 256, x->device), 256, 0, s>>>(*keys, slots, kKeyEmpty);
+  KVX_LAUNCH_CHECK("fill_i64");
+  return KVX_OK;
+}
+
+int read_counters(kvx_index* x, cudaStream_t s, Counters* h) {
+  KVX_CUDA(cudaMemcpyAsync(h, x->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+  KVX_CUDA(cudaStreamSynchronize(s));
+  return KVX_OK;
+}
+
+int rebuild(kvx_index* x, int64_t new_slots, cudaStream_t s) {
+  int64_t *nk = nullptr, *nv = nullptr;
+  int st = alloc_table(x, new_slots, s, &nk, &nv);
+  if (st) return st;
+  KVX_CUDA(cudaMemsetAsync(x->ctr, 0, 2 * sizeof(unsigned long long), s));  // live, used
+  if (x->keys) {
+    rehash_kernel<<<grid_for(x->slots, 256, x->device), 256, 0, s>>>(
+        x->keys, x->vals, x->slots, nk, nv, static_cast<uint64_t>(new_slots - 1), x->ctr);
+    KVX_LAUNCH_CHECK("rehash_kernel");
+    KVX_CUDA(cudaFreeAsync(x->keys, s));
+    KVX_CUDA(cudaFreeAsync(x->vals, s));
+  }
+  x->keys = nk;
+  x->vals = nv;
+  x->slots = new_slots;
+  return KVX_OK;
+}
+
+// Ensure n more keys fit under kMaxLoad.  Only syncs when the cheap upper
+// bound says the table might be too full.
+int ensure_room(kvx_index* x, int64_t n, cudaStream_t s) {
+  if (static_cast<double>(x->used_ub + n) <= kMaxLoad * static_cast<double>(x->slots))
+    return KVX_OK;
+  Counters h;
+  int st = read_counters(x, s, &h);
+  if (st) return st;
+  const int64_t live = static_cast<int64_t>(h.live), used = static_cast<int64_t>(h.used);
+  x->used_ub = used;
+  if (static_cast<double>(used + n) <= kMaxLoad * static_cast<double>(x->slots)) return KVX_OK;
+  int64_t want = x->slots;
+  while (static_cast<double>(live + n) > kTargetLoad * static_cast<double>(want)) want <<= 1;
+  st = rebuild(x, want, s);
+  if (st) return st;
+  x->used_ub = live;
+  return KVX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kvx_index_create(int device, int64_t capacity_hint, kvx_index** out) {
+  KVX_REQUIRE(out != nullptr, "kvx_index_create: out is NULL");
+  KVX_REQUIRE(capacity_hint >= 0, "kvx_index_create: capacity_hint must be >= 0");
+  int ndev = 0;
+  KVX_CUDA(cudaGetDeviceCount(&ndev));
+  KVX_REQUIRE(device >= 0 && device < ndev, "kvx_index_create: bad device");
+  DeviceGuard g(device);
+  auto* x = new kvx_index();
+  x->device = device;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&x->ctr), sizeof(Counters));
+  if (e != cudaSuccess) {
+    delete x;
+    return cuda_error(e, "kvx_index_create: cudaMalloc(counters)");
+  }
+  cudaMemset(x->ctr, 0, sizeof(Counters));
+  int64_t slots = next_pow2(static_cast<int64_t>(static_cast<double>(capacity_hint) / kTargetLoad) + 1);
+  int st = rebuild(x, slots, nullptr);
+  if (st == KVX_OK) {
+    e = cudaStreamSynchronize(nullptr);
+    if (e != cudaSuccess) st = cuda_error(e, "kvx_index_create");
+  }
+  if (st) {
+    kvx_index_destroy(x);
+    return st;
+  }
+  *out = x;
+  return KVX_OK;
+}
+
+int kvx_index_destroy(kvx_index* x) {
+  if (!x) return KVX_OK;
+  DeviceGuard g(x->device);
+  cudaDeviceSynchronize();
+  if (x->keys) cudaFreeAsync(x->keys, nullptr);
+  if (x->vals) cudaFreeAsync(x->vals, nullptr);
+  if (x->ctr) cudaFree(x->ctr);
+  cudaStreamSynchronize(nullptr);
+  delete x;
+  return KVX_OK;
+}
+
+int kvx_index_device(const kvx_index* x) { return x ? x->device : -1; }
+
+int kvx_index_insert(kvx_index* x, const int64_t* d_keys, const int64_t* d_values, int64_t n,
+                     void* stream) {
+  KVX_REQUIRE(x != nullptr, "kvx_index_insert: NULL index");
+  KVX_REQUIRE(n >= 0, "kvx_index_insert: n must be >= 0");
+  if (n == 0) return KVX_OK;
+  KVX_REQUIRE(d_keys != nullptr, "kvx_index_insert: NULL keys");
+  DeviceGuard g(x->device);
+  cudaStream_t s = as_stream(stream);
+  int st = ensure_room(x, n, s);
+  if (st) return st;
+  insert_kernel<<<grid_for(n, 256, x->device), 256, 0, s>>>(
+      x->keys, x->vals, static_cast<uint64_t>(x->slots - 1), d_keys, d_values, n, x->ctr);
+  KVX_LAUNCH_CHECK("insert_kernel");
+  x->used_ub += n;
+  return KVX_OK;
+}
+
+int kvx_index_erase(kvx_index* x, const int64_t* d_keys, int64_t n, void* stream) {
+  KVX_REQUIRE(x != nullptr, "kvx_index_erase: NULL index");
+  KVX_REQUIRE(n >= 0, "kvx_index_erase: n must be >= 0");
+  if (n == 0) return KVX_OK;
+  KVX_REQUIRE(d_keys != nullptr, "kvx_index_erase: NULL keys");
+  DeviceGuard g(x->device);
+  erase_kernel<<<grid_for(n, 256, x->device), 256, 0, as_stream(stream)>>>(
+      x->keys, static_cast<uint64_t>(x->slots - 1), d_keys, n, x->ctr);
+  KVX_LAUNCH_CHECK("erase_kernel");
+  return KVX_OK;
+}
+
+int kvx_index_lookup(const kvx_index* x, const int64_t* d_keys, int64_t n, int64_t* d_out,
+                     void* stream) {
+  KVX_REQUIRE(x != nullptr, "kvx_index_lookup: NULL index");
+  KVX_REQUIRE(n >= 0, "kvx_index_lookup: n must be >= 0");
+  if (n == 0) return KVX_OK;
+  KVX_REQUIRE(d_keys && d_out, "kvx_index_lookup: NULL array");
+  DeviceGuard g(x->device);
+  lookup_kernel<<<grid_for(n, 256, x->device), 256, 0, as_stream(stream)>>>(
+      x->keys, x->vals, static_cast<uint64_t>(x->slots - 1), d_keys, n, d_out);
+  KVX_LAUNCH_CHECK("lookup_kernel");
+  return KVX_OK;
+}
+
+int kvx_index_clear(kvx_index* x, void* stream) {
+  KVX_REQUIRE(x != nullptr, "kvx_index_clear: NULL index");
+  DeviceGuard g(x->device);
+  cudaStream_t s = as_stream(stream);
+  fill_i64<<<grid_for(x->slots, 256, x->device), 256, 0, s>>>(x->keys, x->slots, kKeyEmpty);
+  KVX_LAUNCH_CHECK("fill_i64");
+  KVX_CUDA(cudaMemsetAsync(x->ctr, 0, 2 * sizeof(unsigned long long), s));
+  x->used_ub = 0;
+  return KVX_OK;
+}
+
+int kvx_index_reserve(kvx_index* x, int64_t min_keys, void* stream) {
+  KVX_REQUIRE(x != nullptr, "kvx_index_reserve: NULL index");
+  KVX_REQUIRE(min_keys >= 0, "kvx_index_reserve: min_keys must be >= 0");
+  DeviceGuard g(x->device);
+  cudaStream_t s = as_stream(stream);
+  Counters h;
+  int st = read_counters(x, s, &h);
+  if (st) return st;
+  const int64_t live = static_cast<int64_t>(h.live);
+  const int64_t want = next_pow2(static_cast<int64_t>(
+      static_cast<double>(std::max(min_keys, live)) / kTargetLoad) + 1);
+  st = rebuild(x, want, s);
+  if (st) return st;
+  x->used_ub = live;
+  return KVX_OK;
+}
+
+int kvx_index_stats(kvx_index* x, int64_t* live, int64_t* tombstones, int64_t* slots,
+                    int64_t* rejected, void* stream) {
+  KVX_REQUIRE(x != nullptr, "kvx_index_stats: NULL index");
+  DeviceGuard g(x->device);
+  Counters h;
+  int st = read_counters(x, as_stream(stream), &h);
+  if (st) return st;
+  if (live) *live = static_cast<int64_t>(h.live);
+  if (tombstones) *tombstones = static_cast<int64_t>(h.used - h.live);
+  if (slots) *slots = x->slots;
+  if (rejected) *rejected = static_cast<int64_t>(h.rejected);
+  return KVX_OK;
+}
+
+int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+                           const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+                           int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
+                           void* stream) {
+  KVX_REQUIRE(n_inst >= 1, "find_best_prefix_match: empty prefill pool");
+  KVX_REQUIRE(n_inst <= KVX_MAX_INSTANCES, "kvx_match_prefix_batch: too many instances");
+  KVX_REQUIRE(idx != nullptr && inst_ids != nullptr, "kvx_match_prefix_batch: NULL instances");
+  KVX_REQUIRE(n_req >= 0, "kvx_match_prefix_batch: n_req must be >= 0");
+  KVX_REQUIRE((d_best_len == nullptr) == (d_best_id == nullptr),
+              "kvx_match_prefix_batch: best_len and best_id go together");
+  if (n_req == 0) return KVX_OK;
+  KVX_REQUIRE(d_keys && d_key_off, "kvx_match_prefix_batch: NULL keys");
+  MatchParams p{};
+  p.n_inst = static_cast<int32_t>(n_inst);
+  const int dev = idx[0] ? idx[0]->device : -1;
+  for (int64_t i = 0; i < n_inst; ++i) {
+    KVX_REQUIRE(idx[i] != nullptr, "kvx_match_prefix_batch: NULL index");
+    KVX_REQUIRE(idx[i]->device == dev, "kvx_match_prefix_batch: indices on different devices");
+    p.keys[i] = idx[i]->keys;
+    p.mask[i] = static_cast<uint64_t>(idx[i]->slots - 1);
+    p.ids[i] = inst_ids[i];
+  }
+  DeviceGuard g(dev);
+  cudaStream_t s = as_stream(stream);
+  if (d_best_len && n_inst > 1)
+    KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
+  const int threads = 256;
+  const int64_t tasks = n_req * n_inst;
+  const int64_t want = (tasks + (threads / 32) - 1) / (threads / 32);
+  const int64_t cap = static_cast<int64_t>(sm_count(dev)) * 16;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(want, cap)));
+  match_kernel<<<blocks, threads, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out, d_best_len,
+                                          d_best_id);
+  KVX_LAUNCH_CHECK("match_kernel");
+  if (d_best_len && n_inst > 1) {
+    unpack_best_kernel<<<grid_for(n_req, 256, dev), 256, 0, s>>>(d_best_len, d_best_id, n_req);
+    KVX_LAUNCH_CHECK("unpack_best_kernel");
+  }
+  return KVX_OK;
+}
+
+}  // extern "C"
