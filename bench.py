@@ -1,0 +1,631 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 KVCache hot path (BASELINE.json metric).
+
+Primary line: "KVCache layer-wise transfer GB/s (gather+P2P+scatter)" on
+Config 2 (64 requests x 8K tokens, 50% shared prefix, LLaMA2-70B KV shape:
+80 layers, 8 KV heads x 128, fp16, 16-token blocks).  A step moves every
+request's whole KV chain (proj/src/sim_engine.cpp:463-464) prefill -> decode,
+layer by layer, in decode waves of 16 requests.  value = payload bytes of all
+pairs per step / step time (GB/s, 1e9).  Inputs (171.8 GB per pair per step)
+are far larger than L2, so no flush is needed between steps.
+
+Secondary object "match": "prefix-match blocks/s" on Config 4 (4096 Kimi-like
+requests, avg 16K tokens, Zipf sessions, 1M-block instance index): a step is
+batched block hashing (K1) + prefix match (K2) of the whole batch.
+
+  python bench.py [--gpus N --steps K --warmup W]        # N=1 default
+  torchrun --nproc-per-node N bench.py --gpus N ...       # N = 2, 4, 8
+  python bench.py --impl reference                        # CPU reference arm
+
+Ranks [0, N/2) are prefill GPUs, [N/2, N) decode GPUs (cluster.py); N = 1 runs
+both instances on one GPU.  Timing: CUDA events on the launching streams after
+a barrier + synchronize, max over ranks.  The oracle (oracle/) is used only
+for the cpu_baseline leg and the --impl reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GB = 1e9
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="kvx", choices=["kvx", "reference"])
+    ap.add_argument("--mode", default="auto",
+                    choices=["auto", "local_fused", "local_staged", "peer_fused", "peer_ce",
+                             "peer_nccl"])
+    ap.add_argument("--copy-impl", default="lsu", choices=["lsu", "tma"])
+    ap.add_argument("--layers-per-chunk", type=int, default=1)
+    ap.add_argument("--ring", type=int, default=3)
+    ap.add_argument("--requests", type=int, default=64)
+    ap.add_argument("--wave", type=int, default=16, help="decode wave (requests resident at once)")
+    ap.add_argument("--block-size", type=int, default=16)
+    ap.add_argument("--dtype-bytes", type=int, default=2)
+    ap.add_argument("--no-match", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md "clocks" line)
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + write.sum per launch from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(kernel)
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = checker / baseline only)
+
+def cpu_transfer_sample(seconds: float, steps: int = 0, warmup: int = 0):
+    """The CPU path of the same pipeline (no reference implementation exists:
+    SPEC.md:183): per layer, gather a request's slabs into a buffer and scatter
+    them into the decode pool with memcpy (oracle/kvx_oracle.c), on all host
+    threads.  Sample: one 8K-token request (512 blocks x 80 layers, fp16,
+    bs=16), i.e. 2,684,354,560 payload bytes per pass."""
+    from oracle import Oracle
+    o = Oracle()
+    threads = os.cpu_count() or 1
+    L, bs, n = 80, 16, 512
+    slab = bs * 8 * 128 * 2
+    src_slots = dst_slots = n
+    src = np.empty(L * 2 * src_slots * slab, dtype=np.uint8)
+    dst = np.empty(L * 2 * dst_slots * slab, dtype=np.uint8)
+    o.fill_pool(src, 0, L, src_slots, slab, nthreads=threads)
+    dst.fill(0)
+    rng = np.random.default_rng(1)
+    st = rng.permutation(src_slots).astype(np.int32)
+    dt = np.arange(n, dtype=np.int32)
+    buf = np.empty(2 * n * slab, dtype=np.uint8)
+    payload = L * 2 * n * slab
+
+    def one_pass():
+        for layer in range(L):
+            o.gather(src, src_slots, slab, st, layer, layer + 1, buf, nthreads=threads)
+            o.scatter(dst, dst_slots, slab, dt, layer, layer + 1, buf, nthreads=threads)
+
+    for _ in range(max(warmup, 1)):
+        one_pass()
+    times = []
+    t_end = time.perf_counter() + seconds
+    while (steps and len(times) < steps) or (not steps and (time.perf_counter() < t_end
+                                                            or len(times) < 2)):
+        t0 = time.perf_counter()
+        one_pass()
+        times.append(time.perf_counter() - t0)
+    # spot-check the round trip against the generator (parity of the baseline itself)
+    w = dst.view(np.uint64).reshape(L, 2, dst_slots, slab // 8)
+    seed = o.slab_seed(0, 79, 1, int(st[7]))
+    assert int(w[79, 1, 7, 5]) == o.kv_word(seed, 5)
+    return {"value": payload / statistics.median(times) / GB, "unit": "GB/s", "cores": threads,
+            "kind": "port",
+            "sample": "1 request x 8K tokens (512 blocks x 80 layers x K,V, 2.68 GB payload), "
+                      f"per-layer memcpy gather+scatter, {len(times)} passes, median"}, times
+
+
+def cpu_match_sample(mw, seconds: float):
+    """Reference CPU path for stage 1: the reference's own chain_hash folded
+    over each block's tokens, then the reference's find_best_prefix_match over
+    its CachePool holding the same 1M keys (oracle/_ref), request slices on
+    all host threads.  Sample: the first 512 requests of the batch."""
+    from oracle import Oracle, RefLib, ref_available
+    threads = os.cpu_count() or 1
+    n = min(512, mw.n_req)
+    tok_off = mw.tok_off[: n + 1]
+    tokens = mw.tokens[: tok_off[-1]]
+    ko = Oracle.key_offsets(tok_off, mw.block_size)
+    keys = np.zeros(int(ko[-1]), dtype=np.int64)
+    if not ref_available():
+        return None
+    ref = RefLib()
+    pool = ref.pool(None, "lru")
+    pool.insert_many(mw.index_keys)
+    times = []
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 2:
+        t0 = time.perf_counter()
+        ref.block_hash_mt(tokens, tok_off, mw.block_size, ko, keys, threads)
+        bl, bi = ref.match_batch_mt([pool], [0], keys, ko, threads)
+        times.append(time.perf_counter() - t0)
+    return {"value": float(ko[-1]) / statistics.median(times), "unit": "blocks/s",
+            "cores": threads, "kind": "reference",
+            "sample": f"{n} requests ({int(ko[-1])} blocks): kvref chain_hash fold + "
+                      "kvref find_best_prefix_match vs a 1M-key kvref CachePool",
+            "best_len_check": bl[:8].tolist()}
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    base, times = cpu_transfer_sample(0, steps=args.steps, warmup=args.warmup)
+    ms = 1e3 * statistics.median(times)
+    line = {"impl": "reference",
+            "metric": "KVCache layer-wise transfer GB/s (gather+P2P+scatter); prefix-match blocks/s",
+            "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "config2 shape, CPU sample (see cpu_baseline.sample)",
+                       "parallelism": f"host threads x{base['cores']}"},
+            "cpu_baseline": base,
+            "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_kvx(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_00079_b200 as pkg
+    from paper_2407_00079_b200 import kvx
+    from paper_2407_00079_b200.cluster import (exchange_with_peer, max_over_ranks,
+                                               pair_topology, sum_over_ranks)
+    from paper_2407_00079_b200.streamer import (KernelTimer, LocalStream, PeerReceiver,
+                                                PeerSender)
+    from paper_2407_00079_b200.workloads import MatchWorkload, TransferWorkload
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+    role = pair_topology(world, rank)
+    kvx.set_copy_impl(args.copy_impl)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    mode = args.mode
+    if mode == "auto":
+        mode = "local_fused" if role.role == "local" else "peer_fused"
+    if (role.role == "local") != mode.startswith("local"):
+        raise SystemExit(f"mode {mode} does not fit {world} GPU(s)")
+
+    wl = TransferWorkload(n_req=args.requests, wave=args.wave, block_size=args.block_size,
+                          dtype_bytes=args.dtype_bytes)
+    pool_kw = dict(layers=wl.layers, block_size=wl.block_size, heads=wl.heads,
+                   head_dim=wl.head_dim, dtype_bytes=wl.dtype_bytes)
+    max_blocks = wl.wave * wl.blocks
+    src = dst = None
+    if role.role in ("local", "prefill"):
+        src = pkg.KVPool(**pool_kw, slots=wl.src_slots, device=dev)
+        src.fill_synthetic(role.pair)
+    if role.role in ("local", "decode"):
+        dst = pkg.KVPool(**pool_kw, slots=wl.dst_slots, device=dev)
+        dst.tensor_view().zero_()
+
+    # decode block tables come from the decode instance's allocator
+    host_src = [wl.wave_src_table(w) for w in range(wl.n_waves)]
+    host_dst = wl.decode_tables(kvx.SlotAllocator) if dst is not None else None
+
+    if role.role == "local":
+        streamer = LocalStream(src, dst, mode, args.layers_per_chunk, args.ring, max_blocks)
+        streams = streamer.streams()
+        flags = kvx.DeviceBuffer(64, dev)
+        flags.tensor(torch.int64).zero_()
+    elif role.role == "prefill":
+        streamer = PeerSender(src, mode, args.layers_per_chunk, args.ring, max_blocks, role.peer)
+        peer = exchange_with_peer(role, streamer.export())
+        host_dst = peer["tables"]
+        streamer.connect(peer, {**pool_kw, "slots": wl.dst_slots})
+        streams = streamer.streams()
+    else:
+        streamer = PeerReceiver(dst, mode, args.layers_per_chunk, args.ring, max_blocks,
+                                role.peer)
+        exp = streamer.export()
+        exp["tables"] = host_dst
+        peer = exchange_with_peer(role, exp)
+        streamer.connect(peer)
+        streams = streamer.streams()
+
+    dev_src = [torch.as_tensor(t, device=f"cuda:{dev}") for t in host_src]
+    dev_dst = [torch.as_tensor(t, device=f"cuda:{dev}") for t in host_dst]
+    n_chunks = -(-wl.layers // args.layers_per_chunk)
+    step_no = [0]
+
+    def run_wave(w, timer):
+        if role.role == "local":
+            streamer.send_wave(dev_src[w], dev_dst[w], timer)
+        elif role.role == "prefill":
+            streamer.send_wave(dev_src[w], dev_dst[w], timer)
+        else:
+            if mode == "peer_fused":
+                streamer.count_fused_chunks(n_chunks)
+            else:
+                streamer.recv_wave(dev_dst[w], dev_src[w].numel(), timer)
+
+    def end_step():
+        step_no[0] += 1
+        if role.role == "local":
+            # completion word of the step (read back by the e2e leg), ordered
+            # after the last scatter/copy of the step
+            join_streams(streams[0])
+            kvx.signal_write(flags.ptr, step_no[0], stream=streams[0])
+        else:
+            streamer.end_step()
+
+    def step(timer):
+        for w in range(wl.n_waves):
+            run_wave(w, timer)
+        end_step()
+
+    def join_streams(main):
+        for s in streams:
+            if s is not main:
+                e = torch.cuda.Event()
+                e.record(s)
+                main.wait_event(e)
+
+    no_timer = KernelTimer(False)
+    for _ in range(args.warmup):
+        step(no_timer)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- full-size parity property: every destination word of every wave
+    mismatch = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+    checked = 0
+    for w in range(wl.n_waves):
+        run_wave(w, no_timer)
+        end_step()
+        for s in streams:
+            s.synchronize()
+        barrier()
+        if dst is not None:
+            dst.verify(dev_dst[w], role.pair, dev_src[w], 0, wl.layers, counter=mismatch)
+            checked += dev_dst[w].numel() * wl.layers * 2 * wl.slab_bytes
+    torch.cuda.synchronize()
+    bad = int(sum_over_ranks(float(mismatch.item()), f"cuda:{dev}"))
+    checked = int(sum_over_ranks(float(checked), f"cuda:{dev}"))
+    if bad:
+        raise SystemExit(f"PARITY FAILURE: {bad} mismatched 64-bit words")
+    barrier()
+
+    # ---- timed region (device events, max over ranks)
+    main = streams[0]
+    timer = KernelTimer(True)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = pkg.launch_count()
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for s in streams:
+        if s is not main:
+            s.wait_stream(main)
+    e0.record(main)
+    for s in streams:
+        if s is not main:
+            s.wait_event(e0)
+    for _ in range(args.steps):
+        step(timer)
+    join_streams(main)
+    e1.record(main)
+    torch.cuda.synchronize()
+    barrier()
+    launches = pkg.launch_count() - launches0
+    clk = clocks.stop()
+    ms_total = max_over_ranks(e0.elapsed_time(e1), f"cuda:{dev}")
+    launches_all = int(sum_over_ranks(float(launches), f"cuda:{dev}"))
+    payload = wl.payload_bytes() * role.pairs
+    value = payload * args.steps / (ms_total / 1e3) / GB
+    ksum = timer.summary()
+    ksum_all = {"avg_ms": max_over_ranks(ksum["avg_ms"] if ksum else 0.0, f"cuda:{dev}")}
+
+    # ---- e2e: through the public API with HOST block tables every step
+    e2e = None
+    if not args.no_e2e:
+        pin_src = [torch.as_tensor(t).pin_memory() for t in host_src]
+        pin_dst = [torch.as_tensor(np.asarray(t)).pin_memory() for t in host_dst]
+        status = torch.zeros(1, dtype=torch.int64).pin_memory()
+        flag_t = (flags.tensor(torch.int64) if role.role == "local"
+                  else streamer.flags.tensor(torch.int64))
+        h2d = sum(t.numel() * 4 for t in pin_src) + sum(t.numel() * 4 for t in pin_dst)
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(main)
+        for s in streams:
+            if s is not main:
+                s.wait_event(f0)
+        for _ in range(args.steps):
+            with torch.cuda.stream(main):
+                for w in range(wl.n_waves):
+                    dev_src[w].copy_(pin_src[w], non_blocking=True)
+                    dev_dst[w].copy_(pin_dst[w], non_blocking=True)
+            for s in streams:
+                if s is not main:
+                    s.wait_stream(main)
+            step(no_timer)
+            join_streams(main)
+            with torch.cuda.stream(main):
+                status.copy_(flag_t[:1], non_blocking=True)
+        f1.record(main)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1), f"cuda:{dev}")
+        e2e = {"value": payload * args.steps / (e2e_ms / 1e3) / GB, "unit": "GB/s",
+               "h2d_bytes_per_step": int(sum_over_ranks(float(h2d), f"cuda:{dev}")),
+               "d2h_bytes_per_step": int(sum_over_ranks(8.0, f"cuda:{dev}")),
+               "path": "python API -> libkvx C ABI; pinned host block tables H2D + completion "
+                       "word D2H inside the timed region; KV pools resident in HBM"}
+
+    # ---- secondary: prefix match (Config 4), every rank on its own replica
+    match = None
+    if not args.no_match:
+        match = bench_match(args, dev, rank, world, role)
+
+    # release pool memory before the CPU leg
+    del streamer
+    torch.cuda.synchronize()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, _ = cpu_transfer_sample(args.cpu_seconds)
+
+    peaks = measured_peaks()
+    roof = None
+    if ksum:
+        kname = {"local_fused": "copy_lsu_kernel", "local_staged": "copy_lsu_kernel",
+                 "peer_fused": "copy_lsu_kernel", "peer_ce": "copy_lsu_kernel",
+                 "peer_nccl": "copy_lsu_kernel"}[mode]
+        if args.copy_impl == "tma":
+            kname = "copy_tma_kernel"
+        achieved = ksum["avg_algorithmic_bytes"] / (ksum_all["avg_ms"] / 1e3) / GB
+        if mode == "peer_fused":
+            bound, peak, pk_src = "nvlink", 770.0, ("B200_PROFILING.md measured peer copy "
+                                                    "(770 GB/s per direction)")
+        else:
+            bound, peak, pk_src = "hbm", peaks["hbm_gbs"], f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"
+        tr = ncu_traffic(f"{kname}:{mode}:{args.copy_impl}")
+        roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": tr, "kernel": kname,
+                "avg_launch_ms": ksum_all["avg_ms"], "launches_timed": ksum["launches"],
+                "algorithmic_bytes_per_launch": ksum["avg_algorithmic_bytes"],
+                "peak_source": pk_src}
+
+    if rank == 0:
+        line = {
+            "metric": "KVCache layer-wise transfer GB/s (gather+P2P+scatter); "
+                      "prefix-match blocks/s",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (counter-based splitmix64 KV content; generate_workload block ids)",
+            "config": {**wl.describe(), "mode": mode, "copy_impl": args.copy_impl,
+                       "layers_per_chunk": args.layers_per_chunk, "pairs": role.pairs,
+                       "parallelism": ("local (prefill+decode on one GPU)" if world == 1 else
+                                       f"{role.pairs}P->{role.pairs}D pairs"),
+                       "l2": "inputs larger than L2 (171.8 GB/pair/step); no flush needed"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_all,
+            "clocks": clk,
+            "parity": {"checked_bytes": checked, "mismatched_words": bad,
+                       "check": "verify kernel: every decode slab word == synthetic source word"},
+            "match": match,
+        }
+        print(json.dumps(line), flush=True)
+    barrier()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_match(args, dev, rank, world, role):
+    import torch
+
+    import paper_2407_00079_b200 as pkg
+    from paper_2407_00079_b200.cluster import max_over_ranks, sum_over_ranks
+    from paper_2407_00079_b200.streamer import KernelTimer
+    from paper_2407_00079_b200.workloads import MatchWorkload
+
+    mw = MatchWorkload().build()
+    d = f"cuda:{dev}"
+    s = torch.cuda.Stream(dev)
+    with torch.cuda.stream(s):
+        warm_tok = torch.as_tensor(mw.warm_tokens, device=d)
+        warm_off = torch.as_tensor(mw.warm_tok_off, device=d)
+        wkeys, _ = pkg.chain_hash_batch(warm_tok, warm_off, mw.block_size, stream=s)
+        wkeys = wkeys[: mw.pool_keys]
+        filler = torch.as_tensor(mw.filler_keys(mw.pool_keys - wkeys.numel()), device=d)
+        index_keys = torch.cat([wkeys, filler])
+        idx = pkg.BlockIndex(dev, mw.pool_keys)
+        idx.insert(index_keys, stream=s)
+        tokens = torch.as_tensor(mw.tokens, device=d)
+        tok_off = torch.as_tensor(mw.tok_off, device=d)
+        key_off = pkg.kvx.key_offsets(tok_off, mw.block_size)
+        n_blocks = int(key_off[-1].item())
+        keys = torch.empty(n_blocks, dtype=torch.int64, device=d)
+        best_len = torch.empty(mw.n_req, dtype=torch.int64, device=d)
+        best_id = torch.empty(mw.n_req, dtype=torch.int32, device=d)
+    s.synchronize()
+    st = idx.stats()
+    assert st["live"] == mw.pool_keys, st
+    mw.index_keys = index_keys.cpu().numpy()
+
+    th, tm = KernelTimer(True), KernelTimer(True)
+    tok_bytes = mw.tokens.nbytes
+
+    def step(timed):
+        a = th.start(s) if timed else None
+        pkg.chain_hash_batch(tokens, tok_off, mw.block_size, key_off=key_off, keys=keys, stream=s)
+        th.stop(s, a, tok_bytes + 8 * n_blocks)
+        b = tm.start(s) if timed else None
+        pkg.match_prefix_batch([idx], [0], keys, key_off, want_lens=False, stream=s,
+                               out=(None, best_len, best_id))
+        tm.stop(s, b, 0)
+
+    for _ in range(args.warmup):
+        step(False)
+    s.synchronize()
+    # parity spot check against the oracle restatement on the first requests
+    from oracle import Oracle
+    o = Oracle()
+    k_ref, ko_ref = o.block_hash_batch(mw.tokens[: mw.tok_off[8]], mw.tok_off[:9], mw.block_size)
+    assert np.array_equal(keys[: ko_ref[-1]].cpu().numpy(), k_ref), "hash parity"
+    lens_all = best_len.cpu().numpy()
+    n_probes = int(np.minimum(lens_all + 1, np.diff(key_off.cpu().numpy())).sum())
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(args.steps):
+        step(True)
+    e1.record(s)
+    s.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
+    total_blocks = sum_over_ranks(float(n_blocks), d)
+    value = total_blocks / (ms / 1e3)
+    hs, ms_match = th.summary(), tm.summary()
+    match_bytes = 24 * n_probes
+
+    # e2e: host tokens in (pinned), best (len, id) out, every step
+    pin_tok = torch.as_tensor(mw.tokens).pin_memory()
+    out_len = torch.empty(mw.n_req, dtype=torch.int64).pin_memory()
+    out_id = torch.empty(mw.n_req, dtype=torch.int32).pin_memory()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(s)
+    for _ in range(args.steps):
+        with torch.cuda.stream(s):
+            tokens.copy_(pin_tok, non_blocking=True)
+        step(False)
+        with torch.cuda.stream(s):
+            out_len.copy_(best_len, non_blocking=True)
+            out_id.copy_(best_id, non_blocking=True)
+    f1.record(s)
+    s.synchronize()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1), d) / args.steps
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_match_sample(mw, min(args.cpu_seconds, 10.0))
+    peaks = measured_peaks()
+    hash_gbs = hs["avg_algorithmic_bytes"] / (hs["avg_ms"] / 1e3) / GB
+    match_gbs = match_bytes / (ms_match["avg_ms"] / 1e3) / GB
+    return {
+        "metric": "prefix-match blocks/s (batched block hash + prefix match)",
+        "value": value, "unit": "blocks/s", "ms_per_step": ms,
+        "config": {**mw.describe(), "instances": 1, "replicas": world},
+        "kernels": {
+            "block_hash_kernel": {"avg_ms": hs["avg_ms"], "bytes": hs["avg_algorithmic_bytes"],
+                                  "achieved_gbs": hash_gbs,
+                                  "frac_hbm": hash_gbs / peaks["hbm_gbs"]},
+            "match_kernel": {"avg_ms": ms_match["avg_ms"], "probes": n_probes,
+                             "bytes": match_bytes, "achieved_gbs": match_gbs,
+                             "frac_hbm": match_gbs / peaks["hbm_gbs"],
+                             "note": "24 B per probed block (8 B query + 16 B slot); the 16 MB "
+                                     "key array is L2-resident, so frac can exceed 1"}},
+        "e2e": {"value": total_blocks / (e2e_ms / 1e3), "unit": "blocks/s",
+                "h2d_bytes_per_step": int(tok_bytes), "d2h_bytes_per_step": mw.n_req * 12},
+        "cpu_baseline": cpu,
+    }
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_kvx(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -196,7 +196,26 @@ int kvx_transfer_query(kvx_xfer* x, uint64_t ticket);
  * transfer queue, ordered after every copy submitted before it. */
 int kvx_transfer_signal(kvx_xfer* x, void* d_flag, uint64_t value);
 
+/* ---- decode block table: deterministic slot allocator (host) ---------- */
+
+/* The decode instance's paged block table.  take() hands out the n lowest
+ * free slots in ascending order (nothing is taken and KVX_ENOMEM returned
+ * when fewer than n are free); the reference has no decode block table
+ * (sim_engine.cpp:161-175 counts tokens only), so this is build-defined and
+ * restated by oracle/kvx_oracle.c:kvo_alloc_lowest_free. */
+typedef struct kvx_slot_alloc kvx_slot_alloc;
+int kvx_slot_alloc_create(int64_t slots, kvx_slot_alloc** out);
+int kvx_slot_alloc_destroy(kvx_slot_alloc* a);
+int64_t kvx_slot_alloc_free_count(const kvx_slot_alloc* a);
+int kvx_slot_alloc_take(kvx_slot_alloc* a, int64_t n, int32_t* table_out);
+int kvx_slot_alloc_mark(kvx_slot_alloc* a, const int32_t* slots, int64_t n);
+int kvx_slot_alloc_release(kvx_slot_alloc* a, const int32_t* slots, int64_t n);
+
 /* ---- cross-process plumbing (one process per GPU) ---------------------- */
+
+/* Raw device allocation (cudaMalloc: exportable with kvx_ipc_export). */
+int kvx_device_alloc(int device, int64_t bytes, void** d_ptr);
+int kvx_device_free(int device, void* d_ptr);
 
 #define KVX_IPC_HANDLE_BYTES 64
 int kvx_ipc_export(void* d_ptr, uint8_t handle[KVX_IPC_HANDLE_BYTES]);

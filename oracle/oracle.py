@@ -205,6 +205,11 @@ class RefLib:
         L.kvref_match_batch_mt.restype = None
         L.kvref_match_batch_mt.argtypes = [C.POINTER(C.c_void_p), _i32p, C.c_int64, _i64p, _i64p,
                                            C.c_int64, _i64p, _i32p, C.c_int]
+        L.kvref_block_hash_mt.restype = None
+        L.kvref_block_hash_mt.argtypes = [_i32p, _i64p, C.c_int64, C.c_int64, _i64p, _i64p,
+                                          C.c_int]
+        L.kvref_pool_insert_many.restype = None
+        L.kvref_pool_insert_many.argtypes = [C.c_void_p, _i64p, C.c_int64]
         L.kvref_estimate_transfer_time.restype = C.c_double
         L.kvref_estimate_transfer_time.argtypes = [C.c_int64, C.c_double, C.c_double,
                                                    C.c_double, C.c_double]
@@ -226,6 +231,14 @@ class RefLib:
         if rc != 0:
             raise ValueError("ValidationError: empty prefill pool")
         return int(bl.value), int(bi.value)
+
+    def block_hash_mt(self, tokens, tok_off, bs, key_off, keys_out, nthreads):
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        to = np.ascontiguousarray(tok_off, dtype=np.int64)
+        ko = np.ascontiguousarray(key_off, dtype=np.int64)
+        self.L.kvref_block_hash_mt(_p(t, _i32p), _p(to, _i64p), len(to) - 1, bs, _p(ko, _i64p),
+                                   _p(keys_out, _i64p), nthreads)
+        return keys_out
 
     def match_batch_mt(self, pools, ids, keys, key_off, nthreads):
         arr = (C.c_void_p * len(pools))(*[p.h for p in pools])
@@ -273,6 +286,10 @@ class RefPool:
         n_ev = self.lib.L.kvref_pool_insert_replicated(self.h, _p(k, _i64p), len(k), chain_offset,
                                                        _p(ev, _i64p), cap)
         return ev[:n_ev].tolist()
+
+    def insert_many(self, keys):
+        k = np.ascontiguousarray(keys, dtype=np.int64)
+        self.lib.L.kvref_pool_insert_many(self.h, _p(k, _i64p), len(k))
 
     def match_prefix(self, keys) -> int:
         k = np.ascontiguousarray(keys, dtype=np.int64)

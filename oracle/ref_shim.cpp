@@ -19,6 +19,7 @@
  *   find_best_prefix_match     proj/src/conductor.cpp:57-73
  *   estimate_transfer_time     proj/src/perf_model.cpp:51-59
  */
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <exception>
@@ -150,6 +151,43 @@ void kvref_match_batch_mt(void* const* pools, const int32_t* ids, int64_t n_inst
   for (int t = 0; t < nthreads; ++t)
     th.emplace_back(work, n_req * t / nthreads, n_req * (t + 1) / nthreads);
   for (auto& x : th) x.join();
+}
+
+/* CPU baseline for stage 1a: prefix block keys folded with the reference's
+ * own chain_hash (the content hash -- a fold over the block's token ids -- is
+ * build-defined), request slices on nthreads std::threads. */
+void kvref_block_hash_mt(const int32_t* tokens, const int64_t* tok_off, int64_t n_req, int64_t bs,
+                         const int64_t* key_off, int64_t* keys, int nthreads) {
+  auto work = [&](int64_t lo, int64_t hi) {
+    for (int64_t r = lo; r < hi; ++r) {
+      int64_t key = 0;
+      int64_t k = key_off[r];
+      for (int64_t t = tok_off[r]; t < tok_off[r + 1]; t += bs) {
+        const int64_t end = std::min(t + bs, tok_off[r + 1]);
+        kvref::BlockId c = 0;
+        for (int64_t i = t; i < end; ++i)
+          c = kvref::chain_hash(c, static_cast<uint64_t>(static_cast<uint32_t>(tokens[i])));
+        key = kvref::chain_hash(key, static_cast<uint64_t>(c));
+        keys[k++] = key;
+      }
+    }
+  };
+  if (nthreads <= 1) {
+    work(0, n_req);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t)
+    th.emplace_back(work, n_req * t / nthreads, n_req * (t + 1) / nthreads);
+  for (auto& x : th) x.join();
+}
+
+/* Bulk-load a reference pool (setup for the CPU baseline; not timed). */
+void kvref_pool_insert_many(void* pool, const int64_t* keys, int64_t n) {
+  auto* p = static_cast<kvref::CachePool*>(pool);
+  const int64_t step = 4096;
+  for (int64_t i = 0; i < n; i += step)
+    p->insert_replicated(span_of(keys + i, std::min(step, n - i)), 0);
 }
 
 double kvref_estimate_transfer_time(int64_t tokens, double kv_bytes_per_token,

@@ -109,6 +109,14 @@ _sig("kvx_ipc_close", C.c_int, _vp)
 _sig("kvx_enable_peer", C.c_int, C.c_int, C.c_int)
 _sig("kvx_signal_write", C.c_int, _vp, _vp, C.c_uint64)
 _sig("kvx_signal_wait", C.c_int, _vp, _vp, C.c_uint64)
+_sig("kvx_device_alloc", C.c_int, C.c_int, _i64, C.POINTER(_vp))
+_sig("kvx_device_free", C.c_int, C.c_int, _vp)
+_sig("kvx_slot_alloc_create", C.c_int, _i64, C.POINTER(_vp))
+_sig("kvx_slot_alloc_destroy", C.c_int, _vp)
+_sig("kvx_slot_alloc_free_count", _i64, _vp)
+_sig("kvx_slot_alloc_take", C.c_int, _vp, _i64, C.POINTER(_i32))
+_sig("kvx_slot_alloc_mark", C.c_int, _vp, C.POINTER(_i32), _i64)
+_sig("kvx_slot_alloc_release", C.c_int, _vp, C.POINTER(_i32), _i64)
 
 
 class KvxError(RuntimeError):
@@ -409,6 +417,66 @@ def signal_write(flag_ptr: int, value: int, stream=None) -> None:
 
 def signal_wait(flag_ptr: int, value: int, stream=None) -> None:
     check(_L.kvx_signal_wait(_vp(_stream(stream)), _vp(flag_ptr), value))
+
+
+class DeviceBuffer:
+    """Raw cudaMalloc'd bytes (IPC-exportable), optionally viewed as a tensor."""
+
+    def __init__(self, nbytes: int, device: int = 0):
+        p = _vp()
+        check(_L.kvx_device_alloc(device, nbytes, C.byref(p)))
+        self.ptr = int(p.value)
+        self.nbytes = nbytes
+        self.device = device
+
+    def close(self):
+        if getattr(self, "ptr", 0):
+            _L.kvx_device_free(self.device, _vp(self.ptr))
+            self.ptr = 0
+
+    __del__ = close
+
+    def tensor(self, dtype=torch.uint8) -> torch.Tensor:
+        t = _wrap_device_bytes(self.ptr, self.nbytes, self.device, owner=self)
+        return t.view(dtype)
+
+
+class SlotAllocator:
+    """Decode-side block table allocator: n lowest free slots, ascending."""
+
+    def __init__(self, slots: int):
+        h = _vp()
+        check(_L.kvx_slot_alloc_create(slots, C.byref(h)))
+        self.h = h
+        self.slots = slots
+
+    def close(self):
+        if getattr(self, "h", None):
+            _L.kvx_slot_alloc_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    @property
+    def free(self) -> int:
+        return int(_L.kvx_slot_alloc_free_count(self.h))
+
+    def take(self, n: int, out=None):
+        import numpy as np
+        if out is None:
+            out = np.empty(max(n, 1), dtype=np.int32)
+        check(_L.kvx_slot_alloc_take(self.h, n, out.ctypes.data_as(C.POINTER(_i32))))
+        return out[:n]
+
+    def mark(self, slots) -> None:
+        import numpy as np
+        a = np.ascontiguousarray(slots, dtype=np.int32)
+        check(_L.kvx_slot_alloc_mark(self.h, a.ctypes.data_as(C.POINTER(_i32)), len(a)))
+
+    def release(self, slots) -> None:
+        import numpy as np
+        a = np.ascontiguousarray(slots, dtype=np.int32)
+        check(_L.kvx_slot_alloc_release(self.h, a.ctypes.data_as(C.POINTER(_i32)), len(a)))
 
 
 def sync(stream=None) -> None:
