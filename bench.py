@@ -474,7 +474,7 @@ def run_kvx(args):
                                                     "(770 GB/s per direction)")
         else:
             bound, peak, pk_src = "hbm", peaks["hbm_gbs"], f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"
-        tr = ncu_traffic(f"{kname}:{mode}:{args.copy_impl}")
+        tr = ncu_traffic(kname)
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": tr, "kernel": kname,
                 "avg_launch_ms": ksum_all["avg_ms"], "launches_timed": ksum["launches"],

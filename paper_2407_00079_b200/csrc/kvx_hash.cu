@@ -5,13 +5,21 @@
 // chained.  The per-block content hash is build-defined: a fold of
 // chain_hash over the block's token ids starting from 0.
 //
-// Mapping: one warp per request.  Each lane folds one block's tokens (the
-// content hash is a serial fold, so a block is the unit of parallelism); the
-// prefix chain across blocks is then a serial fold too, done warp-uniformly
-// over the 32 contents fetched with __shfl_sync, lane j keeping key j.  Token
-// loads are 128-bit when the request's token range is 16-byte aligned and the
-// block size is a multiple of 4; the per-lane stride is bs*4 bytes, so the
-// 32 lanes walk 32 adjacent 64-byte spans and L1 serves the follow-up loads.
+// chain_hash is not associative, so both folds are serial; the parallelism is
+// blocks (content hashes are independent) and requests (key chains are
+// independent).  Two phases, so no lane ever repeats another lane's work:
+//   content_hash_kernel  one warp per request; lane j folds block (32w + j)'s
+//                        tokens and parks the content hash in keys[].  Token
+//                        loads are 128-bit when the request's token range is
+//                        16-byte aligned and bs % 4 == 0 (warp-uniform test),
+//                        scalar otherwise; lanes walk adjacent 4*bs-byte spans
+//                        so L1 serves the follow-up loads of each line.
+//   key_fold_kernel      one LANE per request: key_i = chain_hash(key_{i-1},
+//                        content_i) in place, 8 contents prefetched per step.
+//                        32-thread CTAs spread the (latency-bound) chains over
+//                        every SM.
+// Pure integer work: 64-bit multiplies are IMAD sequences (no native 64-bit
+// multiplier), tensor cores do not apply.
 #include "kvx_common.cuh"
 
 namespace kvx {
@@ -39,11 +47,11 @@ __device__ __forceinline__ int64_t fold_tokens_vec4(const int32_t* __restrict__ 
   return h;
 }
 
-__global__ void __launch_bounds__(256) block_hash_kernel(const int32_t* __restrict__ tokens,
-                                                         const int64_t* __restrict__ tok_off,
-                                                         int64_t n_req, int bs,
-                                                         const int64_t* __restrict__ key_off,
-                                                         int64_t* __restrict__ keys) {
+__global__ void __launch_bounds__(256) content_hash_kernel(const int32_t* __restrict__ tokens,
+                                                           const int64_t* __restrict__ tok_off,
+                                                           int64_t n_req, int bs,
+                                                           const int64_t* __restrict__ key_off,
+                                                           int64_t* __restrict__ keys) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -54,25 +62,37 @@ __global__ void __launch_bounds__(256) block_hash_kernel(const int32_t* __restri
     int64_t* out = keys + key_off[r];
     const bool vec = ((bs & 3) == 0) &&
                      ((reinterpret_cast<uintptr_t>(tokens + lo) & 15) == 0);  // warp-uniform
-    int64_t prev = 0;
-    for (int64_t b0 = 0; b0 < nblk; b0 += 32) {
-      const int64_t b = b0 + lane;
-      uint64_t content = 0;
-      if (b < nblk) {
-        const int64_t t0 = lo + b * bs;
-        const int n = static_cast<int>(min(static_cast<int64_t>(bs), hi - t0));
-        content = static_cast<uint64_t>((vec && n == bs) ? fold_tokens_vec4(tokens + t0, n)
-                                                          : fold_tokens_scalar(tokens + t0, n));
-      }
-      const int cnt = static_cast<int>(min(static_cast<int64_t>(32), nblk - b0));
-      int64_t mine = 0;
-      for (int j = 0; j < cnt; ++j) {
-        const uint64_t c = __shfl_sync(0xffffffffu, content, j);
-        prev = chain_hash(prev, c);
-        if (lane == j) mine = prev;
-      }
-      if (b < nblk) out[b] = mine;
+    for (int64_t b = lane; b < nblk; b += 32) {
+      const int64_t t0 = lo + b * bs;
+      const int n = static_cast<int>(min(static_cast<int64_t>(bs), hi - t0));
+      out[b] = (vec && n == bs) ? fold_tokens_vec4(tokens + t0, n)
+                                : fold_tokens_scalar(tokens + t0, n);
     }
+  }
+}
+
+__global__ void __launch_bounds__(32) key_fold_kernel(const int64_t* __restrict__ key_off,
+                                                      int64_t n_req, int64_t* __restrict__ keys) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= n_req) return;
+  const int64_t k0 = key_off[r], k1 = key_off[r + 1];
+  int64_t prev = 0;
+  int64_t k = k0;
+  for (; k + 8 <= k1; k += 8) {
+    int64_t c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = keys[k + j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      prev = chain_hash(prev, static_cast<uint64_t>(c[j]));
+      c[j] = prev;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) keys[k + j] = c[j];
+  }
+  for (; k < k1; ++k) {
+    prev = chain_hash(prev, static_cast<uint64_t>(keys[k]));
+    keys[k] = prev;
   }
 }
 
@@ -90,13 +110,15 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
   KVX_REQUIRE(d_tok_off && d_key_off && d_keys, "kvx_chain_hash_batch: NULL array");
   int dev = 0;
   KVX_CUDA(cudaGetDevice(&dev));
+  cudaStream_t s = as_stream(stream);
   const int threads = 256;
   const int64_t want = (n_req + (threads / 32) - 1) / (threads / 32);
   const int64_t cap = static_cast<int64_t>(sm_count(dev)) * 8;
   const int blocks = static_cast<int>(want < cap ? want : cap);
-  block_hash_kernel<<<blocks, threads, 0, as_stream(stream)>>>(d_tokens, d_tok_off, n_req,
-                                                               static_cast<int>(bs), d_key_off,
-                                                               d_keys);
-  KVX_LAUNCH_CHECK("block_hash_kernel");
+  content_hash_kernel<<<blocks, threads, 0, s>>>(d_tokens, d_tok_off, n_req, static_cast<int>(bs),
+                                                 d_key_off, d_keys);
+  KVX_LAUNCH_CHECK("content_hash_kernel");
+  key_fold_kernel<<<static_cast<int>((n_req + 31) / 32), 32, 0, s>>>(d_key_off, n_req, d_keys);
+  KVX_LAUNCH_CHECK("key_fold_kernel");
   return KVX_OK;
 }
