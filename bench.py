@@ -315,6 +315,11 @@ def run_kvx(args):
     dev_src = [torch.as_tensor(t, device=f"cuda:{dev}") for t in host_src]
     dev_dst = [torch.as_tensor(t, device=f"cuda:{dev}") for t in host_dst]
     n_chunks = -(-wl.layers // args.layers_per_chunk)
+    link_gbs = None
+    if world > 1:
+        g = probe_link(role, dev)
+        # slowest prefill -> decode link of the box (min over pairs)
+        link_gbs = -max_over_ranks(-(g if g is not None else 1e30), f"cuda:{dev}")
     step_no = [0]
 
     def run_wave(w, timer):
@@ -368,6 +373,9 @@ def run_kvx(args):
         if dst is not None:
             dst.verify(dev_dst[w], role.pair, dev_src[w], 0, wl.layers, counter=mismatch)
             checked += dev_dst[w].numel() * wl.layers * 2 * wl.slab_bytes
+        # the next wave reuses the same decode slots: finish checking first
+        torch.cuda.synchronize()
+        barrier()
     torch.cuda.synchronize()
     bad = int(sum_over_ranks(float(mismatch.item()), f"cuda:{dev}"))
     checked = int(sum_over_ranks(float(checked), f"cuda:{dev}"))
@@ -470,8 +478,8 @@ def run_kvx(args):
             kname = "copy_tma_kernel"
         achieved = ksum["avg_algorithmic_bytes"] / (ksum_all["avg_ms"] / 1e3) / GB
         if mode == "peer_fused":
-            bound, peak, pk_src = "nvlink", 770.0, ("B200_PROFILING.md measured peer copy "
-                                                    "(770 GB/s per direction)")
+            bound, peak, pk_src = "nvlink", link_gbs, ("measured in this run: 1 GiB copy-engine "
+                                                       "peer copy, slowest pair")
         else:
             bound, peak, pk_src = "hbm", peaks["hbm_gbs"], f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"
         tr = ncu_traffic(kname)
@@ -495,6 +503,11 @@ def run_kvx(args):
                                        f"{role.pairs}P->{role.pairs}D pairs"),
                        "l2": "inputs larger than L2 (171.8 GB/pair/step); no flush needed"},
             "roofline": roof,
+            "link": (None if world == 1 else {
+                "achieved_per_pair": value / role.pairs, "peak_per_direction": link_gbs,
+                "frac": value / role.pairs / link_gbs, "unit": "GB/s",
+                "peak_source": "measured in this run: 1 GiB copy-engine peer copy, slowest pair",
+                "nominal": 900.0}),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches_all,
@@ -508,6 +521,38 @@ def run_kvx(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def probe_link(role, dev):
+    """Measured NVLink peer-copy peak of this pair: six 1 GiB copy-engine
+    copies prefill -> decode (first one untimed), CUDA events on the copy
+    queue.  Returns GB/s per direction (prefill ranks), None on decode ranks."""
+    import torch
+
+    from paper_2407_00079_b200 import kvx
+    from paper_2407_00079_b200.cluster import exchange_with_peer
+    nbytes = 1 << 30
+    buf = kvx.DeviceBuffer(nbytes, dev)
+    payload = {"buf": kvx.ipc_export(buf.ptr)} if role.role == "decode" else {}
+    peer = exchange_with_peer(role, payload)
+    gbs = None
+    if role.role == "prefill":
+        dst = kvx.ipc_open(peer["buf"], dev)
+        eng = kvx.TransferEngine(dev)
+        s = torch.cuda.ExternalStream(eng.stream_handle, device=dev)
+        eng.wait(eng.submit(dst, buf.ptr, nbytes))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(5):
+            t = eng.submit(dst, buf.ptr, nbytes)
+        e1.record(s)
+        eng.wait(t)
+        gbs = 5 * nbytes / (e0.elapsed_time(e1) / 1e3) / GB
+        eng.close()
+        kvx.ipc_close(dst)
+    torch.distributed.barrier()
+    buf.close()
+    return gbs
 
 
 def bench_match(args, dev, rank, world, role):

@@ -182,41 +182,45 @@ struct MatchParams {
   int32_t n_inst;
 };
 
-// Two independent probe chains per lane: issue both first loads before
-// resolving either, so each lane keeps two random L2/HBM reads in flight.
-__device__ __forceinline__ void probe2(const int64_t* __restrict__ tk, uint64_t mask,
-                                       int64_t k0, bool v0, int64_t k1, bool v1, bool& h0,
-                                       bool& h1) {
-  bool d0 = !v0 || is_reserved(k0), d1 = !v1 || is_reserved(k1);
-  h0 = false;
-  h1 = false;
-  uint64_t s0 = mix64(static_cast<uint64_t>(k0)) & mask;
-  uint64_t s1 = mix64(static_cast<uint64_t>(k1)) & mask;
-  while (!(d0 && d1)) {
-    const int64_t c0 = d0 ? kKeyEmpty : __ldg(tk + s0);
-    const int64_t c1 = d1 ? kKeyEmpty : __ldg(tk + s1);
-    if (!d0) {
-      if (c0 == k0) {
-        h0 = true;
-        d0 = true;
-      } else if (c0 == kKeyEmpty) {
-        d0 = true;
-      } else {
-        s0 = (s0 + 1) & mask;
+// U independent probe chains per lane: every chain's next slot load is issued
+// before any is resolved, so each lane keeps U random L2/HBM reads in flight.
+template <int U>
+__device__ __forceinline__ void probe_multi(const int64_t* __restrict__ tk, uint64_t mask,
+                                            const int64_t (&k)[U], const bool (&v)[U],
+                                            bool (&hit)[U]) {
+  bool done[U];
+  uint64_t s[U];
+  bool all = true;
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    done[j] = !v[j] || is_reserved(k[j]);
+    hit[j] = false;
+    s[j] = mix64(static_cast<uint64_t>(k[j])) & mask;
+    all = all && done[j];
+  }
+  while (!all) {
+    int64_t c[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) c[j] = done[j] ? kKeyEmpty : __ldg(tk + s[j]);
+    all = true;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (!done[j]) {
+        if (c[j] == k[j]) {
+          hit[j] = true;
+          done[j] = true;
+        } else if (c[j] == kKeyEmpty) {
+          done[j] = true;
+        } else {
+          s[j] = (s[j] + 1) & mask;
+        }
       }
-    }
-    if (!d1) {
-      if (c1 == k1) {
-        h1 = true;
-        d1 = true;
-      } else if (c1 == kKeyEmpty) {
-        d1 = true;
-      } else {
-        s1 = (s1 + 1) & mask;
-      }
+      all = all && done[j];
     }
   }
 }
+
+constexpr int kProbeChains = 4;  // per lane -> 128 query keys per warp step
 
 __device__ __forceinline__ unsigned long long pack_best(int64_t len, int32_t id) {
   // Larger len wins; on equal len the LOWER id must win, so store ~ordered(id).
@@ -244,23 +248,26 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
     const int64_t n = key_off[r + 1] - base;
     const int64_t* __restrict__ q = keys + base;
     int64_t len = 0;
-    for (int64_t k0 = 0;; k0 += 64) {
-      const int64_t j0 = k0 + lane, j1 = k0 + 32 + lane;
-      const bool v0 = j0 < n, v1 = j1 < n;
-      const int64_t q0 = v0 ? __ldg(q + j0) : 0;
-      const int64_t q1 = v1 ? __ldg(q + j1) : 0;
-      bool h0, h1;
-      probe2(tk, mask, q0, v0, q1, v1, h0, h1);
-      const unsigned m0 = __ballot_sync(0xffffffffu, !h0);
-      const unsigned m1 = __ballot_sync(0xffffffffu, !h1);
-      if (m0) {
-        len = k0 + __ffs(m0) - 1;
-        break;
+    for (int64_t k0 = 0;; k0 += 32 * kProbeChains) {
+      int64_t qk[kProbeChains];
+      bool qv[kProbeChains], hit[kProbeChains];
+#pragma unroll
+      for (int j = 0; j < kProbeChains; ++j) {
+        const int64_t idx = k0 + 32 * j + lane;
+        qv[j] = idx < n;
+        qk[j] = qv[j] ? __ldg(q + idx) : 0;
       }
-      if (m1) {
-        len = k0 + 32 + __ffs(m1) - 1;
-        break;
+      probe_multi<kProbeChains>(tk, mask, qk, qv, hit);
+      bool stop = false;
+#pragma unroll
+      for (int j = 0; j < kProbeChains; ++j) {
+        const unsigned miss = __ballot_sync(0xffffffffu, !hit[j]);  // out-of-range = miss
+        if (!stop && miss) {
+          len = k0 + 32 * j + __ffs(miss) - 1;
+          stop = true;
+        }
       }
+      if (stop) break;
     }
     if (lane == 0) {
       if (len_out) len_out[t] = len;
