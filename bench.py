@@ -271,7 +271,7 @@ def run_kvx(args):
 
     mode = args.mode
     if mode == "auto":
-        mode = "local_fused" if role.role == "local" else "peer_fused"
+        mode = "local_fused" if role.role == "local" else "peer_ce"
     if (role.role == "local") != mode.startswith("local"):
         raise SystemExit(f"mode {mode} does not fit {world} GPU(s)")
 
