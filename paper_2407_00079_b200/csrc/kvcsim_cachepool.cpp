@@ -1,0 +1,416 @@
+// kvcsim_cachepool.cpp -- the GPU-backed kvcsim::CachePool (drop-in block
+// manager; public API in include/kvcsim/kvcache.hpp).
+//
+// Semantics follow the reference block manager exactly
+// (/root/reference/proj/src/kvcache.cpp):
+//   * victim order: LRU by last use; LFU by (use count, last use);
+//     LengthAware by (deepest position first, use count, last use); BlockId
+//     breaks remaining ties (kvcache.cpp:48-63);
+//   * a touch or an insert advances the logical clock (kvcache.cpp:65-70,90-96);
+//   * the chain being admitted is never a victim, including its skip range
+//     (kvcache.cpp:106-111); when every resident block is protected the miss
+//     is counted but nothing is inserted (kvcache.cpp:84,89);
+//   * admit: positions >= capacity are truncated misses (kvcache.cpp:124-127);
+//     insert_replicated: resident blocks are skipped, a position >= capacity
+//     stops the landing (kvcache.cpp:140-146).
+// The structures are this file's own: protection is an epoch stamp on the
+// entry (no per-call map of the chain), victims come from an ordered set of
+// (rank, id) keys.  Residency queries (match_prefix, contains) are kernels on
+// the B200 block index (libkvx: kvx_match_prefix_batch / kvx_index_lookup);
+// every put mirrors its inserted and evicted ids into that index.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "kvcsim/kvcache.hpp"
+#include "kvcsim/kvx_batch.hpp"
+#include "kvx.h"
+
+#if __has_include("kvcsim/errors.hpp")
+#include "kvcsim/errors.hpp"
+#else
+namespace kvcsim {
+class ValidationError : public std::runtime_error {
+ public:
+  explicit ValidationError(const std::string& what) : std::runtime_error(what) {}
+};
+}  // namespace kvcsim
+#endif
+
+#if __has_include("kvcsim/trace.hpp")
+#include "kvcsim/trace.hpp"
+#define KVCSIM_HAVE_TRACE 1
+#endif
+
+namespace kvcsim {
+
+BlockId chain_hash(BlockId prev_key, std::uint64_t content_hash) {
+  return kvx_chain_hash(prev_key, content_hash);
+}
+
+const char* to_string(CachePolicy policy) {
+  switch (policy) {
+    case CachePolicy::kLru: return "lru";
+    case CachePolicy::kLfu: return "lfu";
+    case CachePolicy::kLengthAware: return "length_aware";
+  }
+  return "?";
+}
+
+std::optional<CachePolicy> cache_policy_from_string(const std::string& name) {
+  static const std::map<std::string, CachePolicy> kNames = {
+      {"lru", CachePolicy::kLru}, {"lfu", CachePolicy::kLfu},
+      {"length_aware", CachePolicy::kLengthAware}};
+  const auto it = kNames.find(name);
+  if (it == kNames.end()) return std::nullopt;
+  return it->second;
+}
+
+// ---------------------------------------------------------------------------
+namespace gpu {
+
+[[noreturn]] void fail(int st, const char* what) {
+  throw std::runtime_error(std::string("kvcsim gpu: ") + what + ": " + kvx_last_error() +
+                           " (status " + std::to_string(st) + ")");
+}
+
+inline void ok(int st, const char* what) {
+  if (st != KVX_OK) fail(st, what);
+}
+
+inline void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string("kvcsim gpu: ") + what + ": " + cudaGetErrorString(e));
+}
+
+int selected_device() {
+  static const int dev = [] {
+    const char* env = std::getenv("KVCSIM_CUDA_DEVICE");
+    return env ? std::atoi(env) : 0;
+  }();
+  return dev;
+}
+
+// One non-blocking stream per process for all pools (pools are single-owner
+// and the engine is single-threaded, so one in-order queue suffices).
+cudaStream_t shared_stream() {
+  static std::once_flag once;
+  static cudaStream_t s = nullptr;
+  std::call_once(once, [] {
+    cuda_ok(cudaSetDevice(selected_device()), "cudaSetDevice");
+    cuda_ok(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+  });
+  return s;
+}
+
+class DeviceIndex {
+ public:
+  DeviceIndex() : dev_(selected_device()), stream_(shared_stream()) {
+    ok(kvx_index_create(dev_, 0, &idx_), "kvx_index_create");
+  }
+  ~DeviceIndex() {
+    if (idx_) kvx_index_destroy(idx_);
+    if (d_buf_) cudaFree(d_buf_);
+    if (h_buf_) cudaFreeHost(h_buf_);
+  }
+  DeviceIndex(const DeviceIndex&) = delete;
+  DeviceIndex& operator=(const DeviceIndex&) = delete;
+
+  const kvx_index* handle() const { return idx_; }
+
+  void apply(const std::vector<BlockId>& erase, const std::vector<BlockId>& insert) {
+    if (erase.empty() && insert.empty()) return;
+    const std::size_t ne = erase.size(), ni = insert.size();
+    stage(ne + ni);
+    std::memcpy(h_buf_, erase.data(), ne * sizeof(int64_t));
+    std::memcpy(h_buf_ + ne, insert.data(), ni * sizeof(int64_t));
+    cuda_ok(cudaMemcpyAsync(d_buf_, h_buf_, (ne + ni) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                            stream_), "H2D keys");
+    if (ne) ok(kvx_index_erase(idx_, d_buf_, static_cast<int64_t>(ne), stream_), "erase");
+    if (ni) ok(kvx_index_insert(idx_, d_buf_ + ne, nullptr, static_cast<int64_t>(ni), stream_),
+               "insert");
+    // h_buf_ is reused by the next call: the copy must have consumed it.
+    cuda_ok(cudaStreamSynchronize(stream_), "apply sync");
+  }
+
+  std::size_t match(std::span<const BlockId> blocks) const {
+    if (blocks.empty()) return 0;
+    const std::size_t n = blocks.size();
+    stage(n + 3);
+    h_buf_[0] = 0;
+    h_buf_[1] = static_cast<int64_t>(n);
+    std::memcpy(h_buf_ + 2, blocks.data(), n * sizeof(int64_t));
+    cuda_ok(cudaMemcpyAsync(d_buf_, h_buf_, (n + 2) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                            stream_), "H2D query");
+    const int32_t id = 0;
+    const kvx_index* one[1] = {idx_};
+    int64_t* d_len = d_buf_ + n + 2;
+    ok(kvx_match_prefix_batch(one, &id, 1, d_buf_ + 2, d_buf_, 1, d_len, nullptr, nullptr,
+                              stream_), "match_prefix");
+    cuda_ok(cudaMemcpyAsync(h_buf_ + n + 2, d_len, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            stream_), "D2H len");
+    cuda_ok(cudaStreamSynchronize(stream_), "match sync");
+    return static_cast<std::size_t>(h_buf_[n + 2]);
+  }
+
+  bool contains(BlockId id) const {
+    stage(2);
+    h_buf_[0] = id;
+    cuda_ok(cudaMemcpyAsync(d_buf_, h_buf_, sizeof(int64_t), cudaMemcpyHostToDevice, stream_),
+            "H2D key");
+    ok(kvx_index_lookup(idx_, d_buf_, 1, d_buf_ + 1, stream_), "lookup");
+    cuda_ok(cudaMemcpyAsync(h_buf_ + 1, d_buf_ + 1, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            stream_), "D2H value");
+    cuda_ok(cudaStreamSynchronize(stream_), "contains sync");
+    return h_buf_[1] >= 0;
+  }
+
+ private:
+  void stage(std::size_t words) const {
+    if (words <= cap_) return;
+    std::size_t cap = std::max<std::size_t>(256, cap_);
+    while (cap < words) cap *= 2;
+    if (d_buf_) cudaFree(d_buf_);
+    if (h_buf_) cudaFreeHost(h_buf_);
+    d_buf_ = nullptr;
+    h_buf_ = nullptr;
+    cuda_ok(cudaMalloc(reinterpret_cast<void**>(&d_buf_), cap * sizeof(int64_t)), "cudaMalloc");
+    cuda_ok(cudaMallocHost(reinterpret_cast<void**>(&h_buf_), cap * sizeof(int64_t)),
+            "cudaMallocHost");
+    cap_ = cap;
+  }
+
+  int dev_;
+  cudaStream_t stream_;
+  kvx_index* idx_ = nullptr;
+  mutable int64_t* d_buf_ = nullptr;
+  mutable int64_t* h_buf_ = nullptr;
+  mutable std::size_t cap_ = 0;
+};
+
+}  // namespace gpu
+
+// ---------------------------------------------------------------------------
+
+CachePool::CachePool(std::optional<std::size_t> capacity_blocks, CachePolicy policy)
+    : capacity_(capacity_blocks), policy_(policy) {
+  if (capacity_ && *capacity_ == 0)
+    throw ValidationError("cache capacity must be >= 1 block (or unbounded)");
+  dev_ = std::make_unique<gpu::DeviceIndex>();
+}
+
+CachePool::~CachePool() = default;
+CachePool::CachePool(CachePool&&) noexcept = default;
+CachePool& CachePool::operator=(CachePool&&) noexcept = default;
+
+const void* CachePool::device_index() const { return dev_->handle(); }
+
+CachePool::OrderKey CachePool::order_key(BlockId id, const Entry& e) const {
+  const auto lu = static_cast<std::int64_t>(e.last_use);
+  const auto uc = static_cast<std::int64_t>(e.use_count);
+  switch (policy_) {
+    case CachePolicy::kLru: return {lu, 0, 0, id};
+    case CachePolicy::kLfu: return {uc, lu, 0, id};
+    case CachePolicy::kLengthAware: return {-static_cast<std::int64_t>(e.position), uc, lu, id};
+  }
+  return {0, 0, 0, id};
+}
+
+void CachePool::reference(BlockId id, Entry& e) {
+  order_.erase(order_key(id, e));
+  e.last_use = ++clock_;
+  ++e.use_count;
+  order_.insert(order_key(id, e));
+}
+
+// Insert `id` at `position`, evicting unguarded victims while the pool is
+// full.  Returns false when no room could be made.
+bool CachePool::place(BlockId id, std::uint32_t position, std::vector<BlockId>& evicted,
+                      std::vector<BlockId>& inserted) {
+  if (capacity_) {
+    while (meta_.size() >= *capacity_) {
+      auto v = order_.begin();
+      while (v != order_.end() && meta_.find(v->id)->second.guard == guard_epoch_) ++v;
+      if (v == order_.end()) return false;  // everything resident is guarded
+      const BlockId victim = v->id;
+      order_.erase(v);
+      meta_.erase(victim);
+      evicted.push_back(victim);
+    }
+  }
+  Entry e;
+  e.last_use = ++clock_;
+  e.use_count = 1;
+  e.position = position;
+  e.guard = guard_epoch_;
+  order_.insert(order_key(id, e));
+  meta_.emplace(id, e);
+  inserted.push_back(id);
+  return true;
+}
+
+void CachePool::sync_device(const std::vector<BlockId>& inserted,
+                            const std::vector<BlockId>& evicted) {
+  dev_->apply(evicted, inserted);
+}
+
+CachePool::AdmitResult CachePool::admit_and_touch(std::span<const BlockId> blocks) {
+  return admit_and_touch(blocks, 0, 0);
+}
+
+CachePool::AdmitResult CachePool::admit_and_touch(std::span<const BlockId> blocks,
+                                                  std::size_t skip_begin, std::size_t skip_end) {
+  AdmitResult r;
+  ++guard_epoch_;
+  for (BlockId id : blocks) {  // the whole chain is protected, skip range included
+    auto it = meta_.find(id);
+    if (it != meta_.end()) it->second.guard = guard_epoch_;
+  }
+  std::vector<BlockId> inserted;
+  for (std::size_t i = 0; i < blocks.size(); ++i) {
+    if (i >= skip_begin && i < skip_end) continue;
+    const BlockId id = blocks[i];
+    auto it = meta_.find(id);
+    if (it != meta_.end()) {
+      ++r.hits;
+      ++stats_.hits;
+      reference(id, it->second);
+      continue;
+    }
+    ++r.misses;
+    ++stats_.misses;
+    if (capacity_ && i >= *capacity_) {
+      r.truncated = true;
+      continue;
+    }
+    place(id, static_cast<std::uint32_t>(i), r.evicted, inserted);
+  }
+  sync_device(inserted, r.evicted);
+  return r;
+}
+
+std::vector<BlockId> CachePool::insert_replicated(std::span<const BlockId> blocks,
+                                                  std::size_t chain_offset) {
+  std::vector<BlockId> evicted, inserted;
+  ++guard_epoch_;
+  for (BlockId id : blocks) {
+    auto it = meta_.find(id);
+    if (it != meta_.end()) it->second.guard = guard_epoch_;
+  }
+  for (std::size_t i = 0; i < blocks.size(); ++i) {
+    const std::size_t position = chain_offset + i;
+    if (meta_.count(blocks[i])) continue;
+    if (capacity_ && position >= *capacity_) break;
+    place(blocks[i], static_cast<std::uint32_t>(position), evicted, inserted);
+  }
+  sync_device(inserted, evicted);
+  return evicted;
+}
+
+std::size_t CachePool::match_prefix(std::span<const BlockId> blocks) const {
+  return dev_->match(blocks);
+}
+
+bool CachePool::contains(BlockId id) const { return dev_->contains(id); }
+
+std::size_t match_prefix(const CachePool& index, std::span<const BlockId> request_blocks) {
+  return index.match_prefix(request_blocks);
+}
+
+#ifdef KVCSIM_HAVE_TRACE
+std::vector<PolicySweepPoint> policy_sweep(const std::vector<RequestRecord>& trace,
+                                           CachePolicy policy,
+                                           std::span<const std::optional<std::size_t>> capacities) {
+  if (capacities.empty()) throw ValidationError("policy_sweep needs at least one capacity");
+  std::vector<PolicySweepPoint> out;
+  for (const auto& cap : capacities) {
+    CachePool pool(cap, policy);
+    for (const auto& rec : trace) pool.admit_and_touch(rec.hash_ids);
+    out.push_back({cap, pool.stats().hit_ratio()});
+  }
+  return out;
+}
+
+std::vector<PopularityPoint> popularity_cdf(const std::vector<RequestRecord>& trace) {
+  std::unordered_map<BlockId, std::uint64_t> refs;
+  for (const auto& rec : trace)
+    for (BlockId id : rec.hash_ids) ++refs[id];
+  if (refs.empty()) return {};
+  std::map<std::uint64_t, std::size_t> by_count;  // hits beyond first insert -> blocks
+  for (const auto& kv : refs) ++by_count[kv.second - 1];
+  std::vector<PopularityPoint> cdf;
+  std::size_t acc = 0;
+  for (const auto& [hits, n] : by_count) {
+    acc += n;
+    cdf.push_back({hits, static_cast<double>(acc) / static_cast<double>(refs.size())});
+  }
+  return cdf;
+}
+#endif
+
+// ---------------------------------------------------------------------------
+// Batched queries (kvcsim/kvx_batch.hpp)
+
+std::vector<BestPrefixMatchBatch> find_best_prefix_match_batch(
+    std::span<const CachePool* const> instances, std::span<const int> instance_ids,
+    std::span<const BlockId> keys, std::span<const std::int64_t> key_offsets,
+    std::vector<std::size_t>* per_instance) {
+  if (instances.empty()) throw ValidationError("find_best_prefix_match: empty prefill pool");
+  if (instances.size() != instance_ids.size())
+    throw ValidationError("find_best_prefix_match_batch: ids and instances differ in length");
+  if (key_offsets.empty()) return {};
+  const std::size_t n_req = key_offsets.size() - 1;
+  const std::size_t n_inst = instances.size();
+  if (n_inst > KVX_MAX_INSTANCES) throw ValidationError("too many instances");
+  std::vector<const kvx_index*> idx(n_inst);
+  std::vector<int32_t> ids(n_inst);
+  for (std::size_t i = 0; i < n_inst; ++i) {
+    idx[i] = static_cast<const kvx_index*>(instances[i]->device_index());
+    ids[i] = instance_ids[i];
+  }
+  cudaStream_t s = gpu::shared_stream();
+  const std::size_t nk = keys.size();
+  // device layout: [key_off n_req+1][keys nk][len n_req*n_inst][best_len n_req][best_id n_req]
+  const std::size_t words = (n_req + 1) + nk + n_req * n_inst + n_req + (n_req + 1) / 2 + 1;
+  int64_t* d = nullptr;
+  gpu::cuda_ok(cudaMallocAsync(reinterpret_cast<void**>(&d), words * sizeof(int64_t), s),
+               "cudaMallocAsync");
+  int64_t* d_off = d;
+  int64_t* d_keys = d_off + (n_req + 1);
+  int64_t* d_len = d_keys + nk;
+  int64_t* d_best = d_len + n_req * n_inst;
+  auto* d_bid = reinterpret_cast<int32_t*>(d_best + n_req);
+  gpu::cuda_ok(cudaMemcpyAsync(d_off, key_offsets.data(), (n_req + 1) * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, s), "H2D offsets");
+  if (nk)
+    gpu::cuda_ok(cudaMemcpyAsync(d_keys, keys.data(), nk * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, s), "H2D keys");
+  gpu::ok(kvx_match_prefix_batch(idx.data(), ids.data(), static_cast<int64_t>(n_inst),
+                                 nk ? d_keys : nullptr, d_off, static_cast<int64_t>(n_req),
+                                 per_instance ? d_len : nullptr, d_best, d_bid, s),
+          "kvx_match_prefix_batch");
+  std::vector<int64_t> best(n_req);
+  std::vector<int32_t> bid(n_req);
+  std::vector<int64_t> lens(per_instance ? n_req * n_inst : 0);
+  gpu::cuda_ok(cudaMemcpyAsync(best.data(), d_best, n_req * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, s), "D2H best");
+  gpu::cuda_ok(cudaMemcpyAsync(bid.data(), d_bid, n_req * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, s), "D2H ids");
+  if (per_instance)
+    gpu::cuda_ok(cudaMemcpyAsync(lens.data(), d_len, lens.size() * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s), "D2H lens");
+  gpu::cuda_ok(cudaFreeAsync(d, s), "cudaFreeAsync");
+  gpu::cuda_ok(cudaStreamSynchronize(s), "sync");
+  std::vector<BestPrefixMatchBatch> out(n_req);
+  for (std::size_t r = 0; r < n_req; ++r) out[r] = {static_cast<std::size_t>(best[r]), bid[r]};
+  if (per_instance) per_instance->assign(lens.begin(), lens.end());
+  return out;
+}
+
+}  // namespace kvcsim
