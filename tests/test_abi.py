@@ -14,18 +14,40 @@ from conftest import ROOT, golden
 
 LIB = os.path.join(ROOT, "paper_2407_00079_b200", "libkvx.so")
 HDR = os.path.join(ROOT, "include", "kvx.h")
+# every C header under include/ and the library that must export it
+C_HEADERS = {"kvx.h": LIB,
+             "kvcsim_c.h": os.path.join(ROOT, "paper_2407_00079_b200", "libkvcsim_gpu.so")}
 
 
 def _ensure_built():
-    if not os.path.exists(LIB):
+    if not all(os.path.exists(p) for p in C_HEADERS.values()):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2407_00079_b200", "csrc")],
                        check=True)
 
 
-def declared_symbols():
-    txt = open(HDR).read()
+def declared_symbols(header=HDR):
+    txt = open(header).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(kvx_[a-z0-9_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b((?:kvx|kvcsim)_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_every_c_header_is_covered():
+    hdrs = sorted(f for f in os.listdir(os.path.join(ROOT, "include")) if f.endswith(".h"))
+    assert hdrs == sorted(C_HEADERS)
+
+
+@pytest.mark.parametrize("header", sorted(C_HEADERS))
+def test_each_header_exported(header):
+    _ensure_built()
+    lib = C_HEADERS[header]
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(re.findall(r"\bT ((?:kvx|kvcsim)_[a-z0-9_]+)\b", out))
+    syms = declared_symbols(os.path.join(ROOT, "include", header))
+    assert syms and not [s for s in syms if s not in exported]
+    handle = C.CDLL(lib)
+    for s in syms:
+        getattr(handle, s)
 
 
 def test_header_declares_the_survey_minimum():
