@@ -8,12 +8,12 @@
 // chain_hash is not associative, so both folds are serial; the parallelism is
 // blocks (content hashes are independent) and requests (key chains are
 // independent).  Two phases, so no lane ever repeats another lane's work:
-//   content_hash_kernel  one warp per request; lane j folds block (32w + j)'s
+//   content_hash_kernel  flattened over all blocks of the batch (32 per warp,
+//                        perfectly balanced); each lane folds one block's
 //                        tokens and parks the content hash in keys[].  Token
-//                        loads are 128-bit when the request's token range is
-//                        16-byte aligned and bs % 4 == 0 (warp-uniform test),
-//                        scalar otherwise; lanes walk adjacent 4*bs-byte spans
-//                        so L1 serves the follow-up loads of each line.
+//                        loads are 128-bit when the block is 16-byte aligned
+//                        and bs % 4 == 0, scalar otherwise; lanes walk
+//                        adjacent 4*bs-byte spans so L1 serves the follow-ups.
 //   key_fold_kernel      one LANE per request: key_i = chain_hash(key_{i-1},
 //                        content_i) in place, 8 contents prefetched per step.
 //                        32-thread CTAs spread the (latency-bound) chains over
@@ -47,52 +47,70 @@ __device__ __forceinline__ int64_t fold_tokens_vec4(const int32_t* __restrict__ 
   return h;
 }
 
+// Flattened over the batch's blocks: warp w owns blocks [32w, 32w + 32) of the
+// concatenated key array, so every warp does the same amount of hashing no
+// matter how request lengths vary.  Lane 0 finds the owning request by binary
+// search over key_off and broadcasts it; lanes past that request's end walk
+// forward (a warp spans at most a few short requests).
 __global__ void __launch_bounds__(256) content_hash_kernel(const int32_t* __restrict__ tokens,
                                                            const int64_t* __restrict__ tok_off,
                                                            int64_t n_req, int bs,
                                                            const int64_t* __restrict__ key_off,
                                                            int64_t* __restrict__ keys) {
   const int lane = threadIdx.x & 31;
+  const int64_t total = key_off[n_req];
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t r = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       r < n_req; r += warps) {
-    const int64_t lo = tok_off[r];
-    const int64_t hi = tok_off[r + 1];
-    const int64_t nblk = (hi - lo + bs - 1) / bs;
-    int64_t* out = keys + key_off[r];
-    const bool vec = ((bs & 3) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(tokens + lo) & 15) == 0);  // warp-uniform
-    for (int64_t b = lane; b < nblk; b += 32) {
-      const int64_t t0 = lo + b * bs;
-      const int n = static_cast<int>(min(static_cast<int64_t>(bs), hi - t0));
-      out[b] = (vec && n == bs) ? fold_tokens_vec4(tokens + t0, n)
-                                : fold_tokens_scalar(tokens + t0, n);
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       32 * w < total; w += warps) {
+    const int64_t g0 = 32 * w;
+    int64_t r = 0;
+    if (lane == 0) {  // last r with key_off[r] <= g0
+      int64_t lo = 0, hi = n_req - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(key_off + mid) <= g0) lo = mid;
+        else hi = mid - 1;
+      }
+      r = lo;
+    }
+    r = __shfl_sync(0xffffffffu, r, 0);
+    const int64_t g = g0 + lane;
+    if (g < total) {
+      while (__ldg(key_off + r + 1) <= g) ++r;
+      const int64_t b = g - __ldg(key_off + r);
+      const int64_t t0 = __ldg(tok_off + r) + b * bs;
+      const int64_t t1 = __ldg(tok_off + r + 1);
+      const int n = static_cast<int>(min(static_cast<int64_t>(bs), t1 - t0));
+      const bool vec = n == bs && ((bs & 3) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(tokens + t0) & 15) == 0);
+      keys[g] = vec ? fold_tokens_vec4(tokens + t0, n) : fold_tokens_scalar(tokens + t0, n);
     }
   }
 }
 
+// One lane per request; contents are prefetched one 8-block batch ahead so
+// the serial chain never waits on memory.
 __global__ void __launch_bounds__(32) key_fold_kernel(const int64_t* __restrict__ key_off,
                                                       int64_t n_req, int64_t* __restrict__ keys) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= n_req) return;
   const int64_t k0 = key_off[r], k1 = key_off[r + 1];
   int64_t prev = 0;
-  int64_t k = k0;
-  for (; k + 8 <= k1; k += 8) {
-    int64_t c[8];
+  int64_t cur[8], nxt[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) c[j] = keys[k + j];
+  for (int j = 0; j < 8; ++j) cur[j] = (k0 + j < k1) ? keys[k0 + j] : 0;
+  for (int64_t k = k0; k < k1; k += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) nxt[j] = (k + 8 + j < k1) ? keys[k + 8 + j] : 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      prev = chain_hash(prev, static_cast<uint64_t>(c[j]));
-      c[j] = prev;
+      if (k + j < k1) {
+        prev = chain_hash(prev, static_cast<uint64_t>(cur[j]));
+        keys[k + j] = prev;
+      }
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) keys[k + j] = c[j];
-  }
-  for (; k < k1; ++k) {
-    prev = chain_hash(prev, static_cast<uint64_t>(keys[k]));
-    keys[k] = prev;
+    for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
   }
 }
 
@@ -112,9 +130,7 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
   KVX_CUDA(cudaGetDevice(&dev));
   cudaStream_t s = as_stream(stream);
   const int threads = 256;
-  const int64_t want = (n_req + (threads / 32) - 1) / (threads / 32);
-  const int64_t cap = static_cast<int64_t>(sm_count(dev)) * 8;
-  const int blocks = static_cast<int>(want < cap ? want : cap);
+  const int blocks = sm_count(dev) * 8;  // 2048 threads per SM, grid-stride over blocks
   content_hash_kernel<<<blocks, threads, 0, s>>>(d_tokens, d_tok_off, n_req, static_cast<int>(bs),
                                                  d_key_off, d_keys);
   KVX_LAUNCH_CHECK("content_hash_kernel");
