@@ -5,25 +5,35 @@
 // chained.  The per-block content hash is build-defined: a fold of
 // chain_hash over the block's token ids starting from 0.
 //
-// chain_hash is not associative, so both folds are serial; the parallelism is
-// blocks (content hashes are independent) and requests (key chains are
-// independent).  Two phases, so no lane ever repeats another lane's work:
-//   content_hash_kernel  flattened over all blocks of the batch (32 per warp,
-//                        perfectly balanced); each lane folds one block's
-//                        tokens and parks the content hash in keys[].  Token
-//                        loads are 128-bit when the block is 16-byte aligned
-//                        and bs % 4 == 0, scalar otherwise; lanes walk
-//                        adjacent 4*bs-byte spans so L1 serves the follow-ups.
-//   key_fold_kernel      one LANE per request: key_i = chain_hash(key_{i-1},
-//                        content_i) in place, 8 contents prefetched per step.
-//                        32-thread CTAs spread the (latency-bound) chains over
-//                        every SM.
-// Pure integer work: 64-bit multiplies are IMAD sequences (no native 64-bit
-// multiplier), tensor cores do not apply.
+//   content_i = fold(chain_hash, tokens of block i, from 0)      (parallel over blocks)
+//   key_i     = chain_hash(key_{i-1}, content_i), key_{-1} = 0     (serial per request)
+//
+// chain_hash is not associative, so the key chain of a request is a strictly
+// serial fold (~100 cycles of dependent int64 arithmetic per block), while the
+// content hashes are independent and ALU-throughput bound.  One persistent,
+// cooperatively launched kernel overlaps the two:
+//   * producer warps hash contents in WINDOW-MAJOR order -- window 0 (blocks
+//     0..31) of every request, then window 1 of every request, ... -- one
+//     (request, window) task per warp, lane = block, 128-bit token loads when
+//     aligned.  Contents are parked in keys[] (chain_hash results are >= 0;
+//     keys[] was pre-filled with -1 by block_hash_prep_kernel);
+//   * one fold warp per CTA: lane = request; it walks its request's keys[]
+//     16 at a time with volatile loads, waits only on entries still -1, and
+//     overwrites each content with the chained key.
+// Window-major production keeps every request's fold right behind its
+// producer, so the batch costs ~max(content throughput, longest fold) instead
+// of their sum.  Waiting happens only inside this single cooperative launch
+// (all CTAs co-resident), never between separate launches.
+#include <algorithm>
+#include <mutex>
+
 #include "kvx_common.cuh"
 
 namespace kvx {
 namespace {
+
+constexpr int kHashThreads = 256;  // 8 warps: warp 0 folds (when assigned), 1..7 produce
+constexpr int kFoldBatch = 16;
 
 __device__ __forceinline__ int64_t fold_tokens_scalar(const int32_t* __restrict__ t, int n) {
   int64_t h = 0;
@@ -47,71 +57,100 @@ __device__ __forceinline__ int64_t fold_tokens_vec4(const int32_t* __restrict__ 
   return h;
 }
 
-// Flattened over the batch's blocks: warp w owns blocks [32w, 32w + 32) of the
-// concatenated key array, so every warp does the same amount of hashing no
-// matter how request lengths vary.  Lane 0 finds the owning request by binary
-// search over key_off and broadcasts it; lanes past that request's end walk
-// forward (a warp spans at most a few short requests).
-__global__ void __launch_bounds__(256) content_hash_kernel(const int32_t* __restrict__ tokens,
-                                                           const int64_t* __restrict__ tok_off,
-                                                           int64_t n_req, int bs,
-                                                           const int64_t* __restrict__ key_off,
-                                                           int64_t* __restrict__ keys) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ int64_t ld_volatile(const int64_t* p) {
+  int64_t v;
+  asm volatile("ld.volatile.global.s64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+// keys[0 .. total) = -1 ("content not ready"); ws[0] = max windows per request.
+__global__ void __launch_bounds__(256) block_hash_prep_kernel(const int64_t* __restrict__ key_off,
+                                                              int64_t n_req,
+                                                              int64_t* __restrict__ keys,
+                                                              unsigned long long* __restrict__ ws) {
   const int64_t total = key_off[n_req];
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-       32 * w < total; w += warps) {
-    const int64_t g0 = 32 * w;
-    int64_t r = 0;
-    if (lane == 0) {  // last r with key_off[r] <= g0
-      int64_t lo = 0, hi = n_req - 1;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(key_off + mid) <= g0) lo = mid;
-        else hi = mid - 1;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = tid; i < total; i += stride) keys[i] = -1;
+  unsigned long long wmax = 0;
+  for (int64_t r = tid; r < n_req; r += stride) {
+    const auto w = static_cast<unsigned long long>((key_off[r + 1] - key_off[r] + 31) / 32);
+    wmax = w > wmax ? w : wmax;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long x = __shfl_down_sync(0xffffffffu, wmax, o);
+    wmax = x > wmax ? x : wmax;
+  }
+  if ((threadIdx.x & 31) == 0 && wmax) atomicMax(ws, wmax);
+}
+
+__global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
+    const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
+    int bs, const int64_t* __restrict__ key_off, int64_t* keys,
+    const unsigned long long* __restrict__ ws, int fold_ctas) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  constexpr int kWarps = kHashThreads / 32;
+  const int cta = static_cast<int>(blockIdx.x);
+
+  if (warp == 0 && cta < fold_ctas) {  // folding warp: lane = request
+    const int64_t lanes = static_cast<int64_t>(fold_ctas) * 32;
+    for (int64_t r = static_cast<int64_t>(cta) * 32 + lane; r < n_req; r += lanes) {
+      const int64_t k0 = key_off[r], k1 = key_off[r + 1];
+      int64_t prev = 0;
+      for (int64_t k = k0; k < k1; k += kFoldBatch) {
+        const int m = static_cast<int>(min(static_cast<int64_t>(kFoldBatch), k1 - k));
+        int64_t c[kFoldBatch];
+#pragma unroll
+        for (int j = 0; j < kFoldBatch; ++j) c[j] = j < m ? ld_volatile(keys + k + j) : 0;
+#pragma unroll
+        for (int j = 0; j < kFoldBatch; ++j) {
+          if (j < m) {
+            while (c[j] < 0) {  // its producer has not reached this block yet
+              __nanosleep(64);
+              c[j] = ld_volatile(keys + k + j);
+            }
+            prev = chain_hash(prev, static_cast<uint64_t>(c[j]));
+            keys[k + j] = prev;
+          }
+        }
       }
-      r = lo;
     }
-    r = __shfl_sync(0xffffffffu, r, 0);
-    const int64_t g = g0 + lane;
-    if (g < total) {
-      while (__ldg(key_off + r + 1) <= g) ++r;
-      const int64_t b = g - __ldg(key_off + r);
-      const int64_t t0 = __ldg(tok_off + r) + b * bs;
-      const int64_t t1 = __ldg(tok_off + r + 1);
-      const int n = static_cast<int>(min(static_cast<int64_t>(bs), t1 - t0));
+    return;
+  }
+
+  // producer warps, numbered densely after removing the folding warps
+  const int64_t pw = static_cast<int64_t>(cta) * kWarps + warp -
+                     min(static_cast<int64_t>(cta + (warp > 0 ? 1 : 0)),
+                         static_cast<int64_t>(fold_ctas));
+  const int64_t producers = static_cast<int64_t>(gridDim.x) * kWarps - fold_ctas;
+  const int64_t tasks = static_cast<int64_t>(ws[0]) * n_req;
+  for (int64_t t = pw; t < tasks; t += producers) {
+    const int64_t w = t / n_req;  // window-major: every request's window w before any w+1
+    const int64_t r = t - w * n_req;
+    const int64_t k0 = key_off[r];
+    const int64_t nblk = key_off[r + 1] - k0;
+    if (w * 32 >= nblk) continue;  // warp-uniform: request shorter than this window
+    const int64_t b = w * 32 + lane;
+    if (b < nblk) {
+      const int64_t t0 = tok_off[r] + b * bs;
+      const int n = static_cast<int>(min(static_cast<int64_t>(bs), tok_off[r + 1] - t0));
       const bool vec = n == bs && ((bs & 3) == 0) &&
                        ((reinterpret_cast<uintptr_t>(tokens + t0) & 15) == 0);
-      keys[g] = vec ? fold_tokens_vec4(tokens + t0, n) : fold_tokens_scalar(tokens + t0, n);
+      keys[k0 + b] = vec ? fold_tokens_vec4(tokens + t0, n) : fold_tokens_scalar(tokens + t0, n);
     }
   }
 }
 
-// One lane per request; contents are prefetched one 8-block batch ahead so
-// the serial chain never waits on memory.
-__global__ void __launch_bounds__(32) key_fold_kernel(const int64_t* __restrict__ key_off,
-                                                      int64_t n_req, int64_t* __restrict__ keys) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (r >= n_req) return;
-  const int64_t k0 = key_off[r], k1 = key_off[r + 1];
-  int64_t prev = 0;
-  int64_t cur[8], nxt[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) cur[j] = (k0 + j < k1) ? keys[k0 + j] : 0;
-  for (int64_t k = k0; k < k1; k += 8) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) nxt[j] = (k + 8 + j < k1) ? keys[k + 8 + j] : 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (k + j < k1) {
-        prev = chain_hash(prev, static_cast<uint64_t>(cur[j]));
-        keys[k + j] = prev;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) cur[j] = nxt[j];
-  }
+struct Workspace {
+  std::mutex mu;
+  unsigned long long* ws[64] = {nullptr};
+  int grid[64] = {0};
+};
+
+Workspace& workspace() {
+  static Workspace w;
+  return w;
 }
 
 }  // namespace
@@ -128,13 +167,32 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
   KVX_REQUIRE(d_tok_off && d_key_off && d_keys, "kvx_chain_hash_batch: NULL array");
   int dev = 0;
   KVX_CUDA(cudaGetDevice(&dev));
+  KVX_REQUIRE(dev < 64, "kvx_chain_hash_batch: device index too large");
   cudaStream_t s = as_stream(stream);
-  const int threads = 256;
-  const int blocks = sm_count(dev) * 8;  // 2048 threads per SM, grid-stride over blocks
-  content_hash_kernel<<<blocks, threads, 0, s>>>(d_tokens, d_tok_off, n_req, static_cast<int>(bs),
-                                                 d_key_off, d_keys);
-  KVX_LAUNCH_CHECK("content_hash_kernel");
-  key_fold_kernel<<<static_cast<int>((n_req + 31) / 32), 32, 0, s>>>(d_key_off, n_req, d_keys);
-  KVX_LAUNCH_CHECK("key_fold_kernel");
+  Workspace& W = workspace();
+  unsigned long long* ws;
+  int grid;
+  {
+    std::lock_guard<std::mutex> lk(W.mu);
+    if (!W.ws[dev]) {
+      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&W.ws[dev]), 64));
+      int per_sm = 0;
+      KVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_hash_fused_kernel,
+                                                             kHashThreads, 0));
+      W.grid[dev] = std::max(1, per_sm) * sm_count(dev);
+    }
+    ws = W.ws[dev];
+    grid = W.grid[dev];
+  }
+  KVX_CUDA(cudaMemsetAsync(ws, 0, sizeof(unsigned long long), s));
+  block_hash_prep_kernel<<<sm_count(dev) * 4, 256, 0, s>>>(d_key_off, n_req, d_keys, ws);
+  KVX_LAUNCH_CHECK("block_hash_prep_kernel");
+  int fold_ctas = static_cast<int>(std::min<int64_t>((n_req + 31) / 32, grid));
+  int bsi = static_cast<int>(bs);
+  void* args[] = {const_cast<int32_t**>(&d_tokens), const_cast<int64_t**>(&d_tok_off), &n_req,
+                  &bsi, const_cast<int64_t**>(&d_key_off), &d_keys, &ws, &fold_ctas};
+  KVX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(block_hash_fused_kernel),
+                                       dim3(grid), dim3(kHashThreads), args, 0, s));
+  KVX_LAUNCH_CHECK("block_hash_fused_kernel");
   return KVX_OK;
 }

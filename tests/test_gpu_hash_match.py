@@ -38,6 +38,18 @@ def test_block_hash_random_vs_oracle(kvx, oracle_lib, bs, misalign):
     assert np.array_equal(keys.cpu().numpy(), want)
 
 
+def test_block_hash_many_small_requests(kvx, oracle_lib):
+    """More requests than folding lanes (each lane folds several requests) and
+    many empty / sub-block requests."""
+    rng = np.random.default_rng(77)
+    lens = rng.integers(0, 60, size=40000)
+    tok_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    tokens = rng.integers(0, 32000, size=int(tok_off[-1])).astype(np.int32)
+    want, _ = oracle_lib.block_hash_batch(tokens, tok_off, 16)
+    keys, _ = kvx.chain_hash_batch(_t(tokens, torch.int32), _t(tok_off, torch.int64), 16)
+    assert np.array_equal(keys.cpu().numpy(), want)
+
+
 def test_scalar_chain_hash(kvx):
     g = golden("chain_hash.npz")
     for p, c, o in zip(g["prev"][:64], g["content"][:64], g["out"][:64]):
