@@ -17,9 +17,11 @@
 //     (request, window) task per warp, lane = block, 128-bit token loads when
 //     aligned.  Contents are parked in keys[] (chain_hash results are >= 0;
 //     keys[] was pre-filled with -1 by block_hash_prep_kernel);
-//   * one fold warp per CTA: lane = request; it walks its request's keys[]
-//     16 at a time with volatile loads, waits only on entries still -1, and
-//     overwrites each content with the chained key.
+//   * folding lanes (lane = request, claimed from a counter) on a few SMs
+//     reserved for them (by %smid) walk their request's keys[] 16 at a time
+//     with volatile loads, wait only on entries still -1, and overwrite each
+//     content with the chained key; producers join the folding when the
+//     content tasks run out.
 // Window-major production keeps every request's fold right behind its
 // producer, so the batch costs ~max(content throughput, longest fold) instead
 // of their sum.  Waiting happens only inside this single cooperative launch
@@ -84,48 +86,62 @@ __global__ void __launch_bounds__(256) block_hash_prep_kernel(const int64_t* __r
   if ((threadIdx.x & 31) == 0 && wmax) atomicMax(ws, wmax);
 }
 
-__global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
-    const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
-    int bs, const int64_t* __restrict__ key_off, int64_t* keys,
-    const unsigned long long* __restrict__ ws, int fold_ctas) {
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  constexpr int kWarps = kHashThreads / 32;
-  const int cta = static_cast<int>(blockIdx.x);
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t id;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
+  return id;
+}
 
-  if (warp == 0 && cta < fold_ctas) {  // folding warp: lane = request
-    const int64_t lanes = static_cast<int64_t>(fold_ctas) * 32;
-    for (int64_t r = static_cast<int64_t>(cta) * 32 + lane; r < n_req; r += lanes) {
-      const int64_t k0 = key_off[r], k1 = key_off[r + 1];
-      int64_t prev = 0;
-      for (int64_t k = k0; k < k1; k += kFoldBatch) {
-        const int m = static_cast<int>(min(static_cast<int64_t>(kFoldBatch), k1 - k));
-        int64_t c[kFoldBatch];
+// Fold whole requests, claimed one per lane from ws[1], until none are left.
+__device__ __forceinline__ void fold_requests(const int64_t* __restrict__ key_off, int64_t n_req,
+                                              int64_t* keys, unsigned long long* ws) {
+  while (true) {
+    const int64_t r = static_cast<int64_t>(atomicAdd(ws + 1, 1ull));
+    if (r >= n_req) return;
+    const int64_t k0 = key_off[r], k1 = key_off[r + 1];
+    int64_t prev = 0;
+    for (int64_t k = k0; k < k1; k += kFoldBatch) {
+      const int m = static_cast<int>(min(static_cast<int64_t>(kFoldBatch), k1 - k));
+      int64_t c[kFoldBatch];
 #pragma unroll
-        for (int j = 0; j < kFoldBatch; ++j) c[j] = j < m ? ld_volatile(keys + k + j) : 0;
+      for (int j = 0; j < kFoldBatch; ++j) c[j] = j < m ? ld_volatile(keys + k + j) : 0;
 #pragma unroll
-        for (int j = 0; j < kFoldBatch; ++j) {
-          if (j < m) {
-            while (c[j] < 0) {  // its producer has not reached this block yet
-              __nanosleep(64);
-              c[j] = ld_volatile(keys + k + j);
-            }
-            prev = chain_hash(prev, static_cast<uint64_t>(c[j]));
-            keys[k + j] = prev;
+      for (int j = 0; j < kFoldBatch; ++j) {
+        if (j < m) {
+          while (c[j] < 0) {  // its producer has not reached this block yet
+            __nanosleep(64);
+            c[j] = ld_volatile(keys + k + j);
           }
+          prev = chain_hash(prev, static_cast<uint64_t>(c[j]));
+          keys[k + j] = prev;
         }
       }
     }
+  }
+}
+
+// Roles by SM: on the first `fold_sms` SMs, the first kFoldWarps warps of each
+// CTA fold (lane = request) and the rest exit, so the latency-bound chains do
+// not compete for issue slots with the ALU-saturated producers; every other
+// warp produces contents, then joins the folding of whatever is unclaimed.
+constexpr int kFoldWarps = 3;
+
+__global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
+    const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
+    int bs, const int64_t* __restrict__ key_off, int64_t* keys, unsigned long long* ws,
+    int fold_sms) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  if (static_cast<int>(sm_id()) < fold_sms) {
+    if (warp < kFoldWarps) fold_requests(key_off, n_req, keys, ws);
     return;
   }
-
-  // producer warps, numbered densely after removing the folding warps
-  const int64_t pw = static_cast<int64_t>(cta) * kWarps + warp -
-                     min(static_cast<int64_t>(cta + (warp > 0 ? 1 : 0)),
-                         static_cast<int64_t>(fold_ctas));
-  const int64_t producers = static_cast<int64_t>(gridDim.x) * kWarps - fold_ctas;
   const int64_t tasks = static_cast<int64_t>(ws[0]) * n_req;
-  for (int64_t t = pw; t < tasks; t += producers) {
+  while (true) {
+    int64_t t = 0;
+    if (lane == 0) t = static_cast<int64_t>(atomicAdd(ws + 2, 1ull));
+    t = __shfl_sync(0xffffffffu, t, 0);
+    if (t >= tasks) break;
     const int64_t w = t / n_req;  // window-major: every request's window w before any w+1
     const int64_t r = t - w * n_req;
     const int64_t k0 = key_off[r];
@@ -140,6 +156,7 @@ __global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
       keys[k0 + b] = vec ? fold_tokens_vec4(tokens + t0, n) : fold_tokens_scalar(tokens + t0, n);
     }
   }
+  fold_requests(key_off, n_req, keys, ws);
 }
 
 struct Workspace {
@@ -184,13 +201,18 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
     ws = W.ws[dev];
     grid = W.grid[dev];
   }
-  KVX_CUDA(cudaMemsetAsync(ws, 0, sizeof(unsigned long long), s));
+  KVX_CUDA(cudaMemsetAsync(ws, 0, 3 * sizeof(unsigned long long), s));
   block_hash_prep_kernel<<<sm_count(dev) * 4, 256, 0, s>>>(d_key_off, n_req, d_keys, ws);
   KVX_LAUNCH_CHECK("block_hash_prep_kernel");
-  int fold_ctas = static_cast<int>(std::min<int64_t>((n_req + 31) / 32, grid));
+  // SMs reserved for folding: about 3 folding warps per SM sub-partition's
+  // worth of lanes per request, at most 1/8 of the chip.
+  const int sms = sm_count(dev);
+  const int64_t lanes_per_fold_sm = static_cast<int64_t>(grid / sms) * kFoldWarps * 32;
+  int fold_sms = static_cast<int>(std::min<int64_t>(
+      std::max<int64_t>(1, (n_req + lanes_per_fold_sm - 1) / lanes_per_fold_sm), sms / 8));
   int bsi = static_cast<int>(bs);
   void* args[] = {const_cast<int32_t**>(&d_tokens), const_cast<int64_t**>(&d_tok_off), &n_req,
-                  &bsi, const_cast<int64_t**>(&d_key_off), &d_keys, &ws, &fold_ctas};
+                  &bsi, const_cast<int64_t**>(&d_key_off), &d_keys, &ws, &fold_sms};
   KVX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(block_hash_fused_kernel),
                                        dim3(grid), dim3(kHashThreads), args, 0, s));
   KVX_LAUNCH_CHECK("block_hash_fused_kernel");
