@@ -137,23 +137,27 @@ __global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
     return;
   }
   const int64_t tasks = static_cast<int64_t>(ws[0]) * n_req;
+  constexpr int64_t kClaim = 8;  // tasks per claim: keeps the shared counter cold
   while (true) {
-    int64_t t = 0;
-    if (lane == 0) t = static_cast<int64_t>(atomicAdd(ws + 2, 1ull));
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= tasks) break;
-    const int64_t w = t / n_req;  // window-major: every request's window w before any w+1
-    const int64_t r = t - w * n_req;
-    const int64_t k0 = key_off[r];
-    const int64_t nblk = key_off[r + 1] - k0;
-    if (w * 32 >= nblk) continue;  // warp-uniform: request shorter than this window
-    const int64_t b = w * 32 + lane;
-    if (b < nblk) {
-      const int64_t t0 = tok_off[r] + b * bs;
-      const int n = static_cast<int>(min(static_cast<int64_t>(bs), tok_off[r + 1] - t0));
-      const bool vec = n == bs && ((bs & 3) == 0) &&
-                       ((reinterpret_cast<uintptr_t>(tokens + t0) & 15) == 0);
-      keys[k0 + b] = vec ? fold_tokens_vec4(tokens + t0, n) : fold_tokens_scalar(tokens + t0, n);
+    int64_t t0 = 0;
+    if (lane == 0) t0 = static_cast<int64_t>(atomicAdd(ws + 2, static_cast<unsigned long long>(kClaim)));
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if (t0 >= tasks) break;
+    const int64_t t_end = min(t0 + kClaim, tasks);
+    for (int64_t t = t0; t < t_end; ++t) {
+      const int64_t w = t / n_req;  // window-major: every request's window w before any w+1
+      const int64_t r = t - w * n_req;
+      const int64_t k0 = key_off[r];
+      const int64_t nblk = key_off[r + 1] - k0;
+      if (w * 32 >= nblk) continue;  // warp-uniform: request shorter than this window
+      const int64_t b = w * 32 + lane;
+      if (b < nblk) {
+        const int64_t tb = tok_off[r] + b * bs;
+        const int n = static_cast<int>(min(static_cast<int64_t>(bs), tok_off[r + 1] - tb));
+        const bool vec = n == bs && ((bs & 3) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(tokens + tb) & 15) == 0);
+        keys[k0 + b] = vec ? fold_tokens_vec4(tokens + tb, n) : fold_tokens_scalar(tokens + tb, n);
+      }
     }
   }
   fold_requests(key_off, n_req, keys, ws);
