@@ -93,6 +93,9 @@ __device__ __forceinline__ uint32_t sm_id() {
 }
 
 // Fold whole requests, claimed one per lane from ws[1], until none are left.
+// The next 16 contents are loaded while the current 16 are chained, so a
+// request whose contents are all produced runs at the chain_hash dependency
+// latency (~97 cycles per block measured, tests/perf/hash_micro.cu).
 __device__ __forceinline__ void fold_requests(const int64_t* __restrict__ key_off, int64_t n_req,
                                               int64_t* keys, unsigned long long* ws) {
   while (true) {
@@ -100,31 +103,39 @@ __device__ __forceinline__ void fold_requests(const int64_t* __restrict__ key_of
     if (r >= n_req) return;
     const int64_t k0 = key_off[r], k1 = key_off[r + 1];
     int64_t prev = 0;
-    for (int64_t k = k0; k < k1; k += kFoldBatch) {
-      const int m = static_cast<int>(min(static_cast<int64_t>(kFoldBatch), k1 - k));
-      int64_t c[kFoldBatch];
+    int64_t c[kFoldBatch];
 #pragma unroll
-      for (int j = 0; j < kFoldBatch; ++j) c[j] = j < m ? ld_volatile(keys + k + j) : 0;
+    for (int j = 0; j < kFoldBatch; ++j) c[j] = (k0 + j < k1) ? ld_volatile(keys + k0 + j) : 0;
+    for (int64_t k = k0; k < k1; k += kFoldBatch) {
+      int64_t nx[kFoldBatch];
+#pragma unroll
+      for (int j = 0; j < kFoldBatch; ++j)
+        nx[j] = (k + kFoldBatch + j < k1) ? ld_volatile(keys + k + kFoldBatch + j) : 0;
+      const int m = static_cast<int>(min(static_cast<int64_t>(kFoldBatch), k1 - k));
 #pragma unroll
       for (int j = 0; j < kFoldBatch; ++j) {
         if (j < m) {
-          while (c[j] < 0) {  // its producer has not reached this block yet
-            __nanosleep(64);
-            c[j] = ld_volatile(keys + k + j);
+          int64_t v = c[j];
+          while (v < 0) {  // its producer has not reached this block yet
+            __nanosleep(32);
+            v = ld_volatile(keys + k + j);
           }
-          prev = chain_hash(prev, static_cast<uint64_t>(c[j]));
+          prev = chain_hash(prev, static_cast<uint64_t>(v));
           keys[k + j] = prev;
         }
       }
+#pragma unroll
+      for (int j = 0; j < kFoldBatch; ++j) c[j] = nx[j];
     }
   }
 }
 
-// Roles by SM: on the first `fold_sms` SMs, the first kFoldWarps warps of each
-// CTA fold (lane = request) and the rest exit, so the latency-bound chains do
-// not compete for issue slots with the ALU-saturated producers; every other
-// warp produces contents, then joins the folding of whatever is unclaimed.
-constexpr int kFoldWarps = 3;
+// Roles by SM: the first CTA to arrive on each of the first `fold_sms` SMs
+// runs kFoldWarps folding warps (one per SM sub-partition: a lone chain runs
+// at its dependency latency, four per sub-partition would be issue bound);
+// other CTAs on those SMs exit.  Every other warp produces contents, then
+// joins the folding of whatever is still unclaimed.
+constexpr int kFoldWarps = 4;
 
 __global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
@@ -132,8 +143,12 @@ __global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
     int fold_sms) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  if (static_cast<int>(sm_id()) < fold_sms) {
-    if (warp < kFoldWarps) fold_requests(key_off, n_req, keys, ws);
+  const int sm = static_cast<int>(sm_id());
+  if (sm < fold_sms) {
+    __shared__ unsigned long long ticket;
+    if (threadIdx.x == 0) ticket = atomicAdd(ws + 3 + sm, 1ull);
+    __syncthreads();
+    if (ticket == 0 && warp < kFoldWarps) fold_requests(key_off, n_req, keys, ws);
     return;
   }
   const int64_t tasks = static_cast<int64_t>(ws[0]) * n_req;
@@ -196,7 +211,8 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
   {
     std::lock_guard<std::mutex> lk(W.mu);
     if (!W.ws[dev]) {
-      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&W.ws[dev]), 64));
+      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&W.ws[dev]),
+                          (3 + sm_count(dev)) * sizeof(unsigned long long)));
       int per_sm = 0;
       KVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_hash_fused_kernel,
                                                              kHashThreads, 0));
@@ -205,15 +221,17 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
     ws = W.ws[dev];
     grid = W.grid[dev];
   }
-  KVX_CUDA(cudaMemsetAsync(ws, 0, 3 * sizeof(unsigned long long), s));
+  // ws: [0] max windows, [1] fold claims, [2] content claims, [3 + sm] per-SM CTA tickets
+  KVX_CUDA(cudaMemsetAsync(ws, 0, (3 + sm_count(dev)) * sizeof(unsigned long long), s));
   block_hash_prep_kernel<<<sm_count(dev) * 4, 256, 0, s>>>(d_key_off, n_req, d_keys, ws);
   KVX_LAUNCH_CHECK("block_hash_prep_kernel");
-  // SMs reserved for folding: about 3 folding warps per SM sub-partition's
-  // worth of lanes per request, at most 1/8 of the chip.
+  // SMs reserved for folding: kFoldWarps * 32 request lanes each, at most a
+  // quarter of the chip (the rest of the requests are folded by producers
+  // once the content tasks are exhausted).
   const int sms = sm_count(dev);
-  const int64_t lanes_per_fold_sm = static_cast<int64_t>(grid / sms) * kFoldWarps * 32;
+  const int64_t lanes_per_fold_sm = static_cast<int64_t>(kFoldWarps) * 32;
   int fold_sms = static_cast<int>(std::min<int64_t>(
-      std::max<int64_t>(1, (n_req + lanes_per_fold_sm - 1) / lanes_per_fold_sm), sms / 8));
+      std::max<int64_t>(1, (n_req + lanes_per_fold_sm - 1) / lanes_per_fold_sm), sms / 4));
   int bsi = static_cast<int>(bs);
   void* args[] = {const_cast<int32_t**>(&d_tokens), const_cast<int64_t**>(&d_tok_off), &n_req,
                   &bsi, const_cast<int64_t**>(&d_key_off), &d_keys, &ws, &fold_sms};
