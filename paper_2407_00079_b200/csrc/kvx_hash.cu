@@ -59,6 +59,45 @@ __device__ __forceinline__ int64_t fold_tokens_vec4(const int32_t* __restrict__ 
   return h;
 }
 
+// 16 tokens starting M tokens into a 16-byte aligned window: five aligned
+// 128-bit loads cover them whatever the block's alignment, and the token
+// selection is resolved at compile time (no per-token address arithmetic).
+template <int M>
+__device__ __forceinline__ int64_t fold16(const int32_t* __restrict__ aligned, int64_t h) {
+  const int4* v = reinterpret_cast<const int4*>(aligned);
+  uint32_t t[20];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    const int4 q = __ldg(v + i);
+    t[4 * i] = static_cast<uint32_t>(q.x);
+    t[4 * i + 1] = static_cast<uint32_t>(q.y);
+    t[4 * i + 2] = static_cast<uint32_t>(q.z);
+    t[4 * i + 3] = static_cast<uint32_t>(q.w);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) h = chain_hash(h, static_cast<uint64_t>(t[M + i]));
+  return h;
+}
+
+// Content hash of a full block whose size is a multiple of 16 tokens; the
+// caller guarantees the 16-byte window [t0 & ~3, t0 & ~3 + bs + 4) is inside
+// the token array.
+__device__ __forceinline__ int64_t fold_tokens_x16(const int32_t* __restrict__ tokens, int64_t t0,
+                                                   int bs) {
+  const int m = static_cast<int>(t0 & 3);
+  const int32_t* a = tokens + (t0 - m);
+  int64_t h = 0;
+  for (int c = 0; c < bs; c += 16, a += 16) {
+    switch (m) {
+      case 0: h = fold16<0>(a, h); break;
+      case 1: h = fold16<1>(a, h); break;
+      case 2: h = fold16<2>(a, h); break;
+      default: h = fold16<3>(a, h); break;
+    }
+  }
+  return h;
+}
+
 __device__ __forceinline__ int64_t ld_volatile(const int64_t* p) {
   int64_t v;
   asm volatile("ld.volatile.global.s64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -152,6 +191,8 @@ __global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
     return;
   }
   const int64_t tasks = static_cast<int64_t>(ws[0]) * n_req;
+  const int64_t total_tok = tok_off[n_req];
+  const bool x16_ok = (bs & 15) == 0 && (reinterpret_cast<uintptr_t>(tokens) & 15) == 0;
   constexpr int64_t kClaim = 8;  // tasks per claim: keeps the shared counter cold
   while (true) {
     int64_t t0 = 0;
@@ -169,9 +210,14 @@ __global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
       if (b < nblk) {
         const int64_t tb = tok_off[r] + b * bs;
         const int n = static_cast<int>(min(static_cast<int64_t>(bs), tok_off[r + 1] - tb));
-        const bool vec = n == bs && ((bs & 3) == 0) &&
-                         ((reinterpret_cast<uintptr_t>(tokens + tb) & 15) == 0);
-        keys[k0 + b] = vec ? fold_tokens_vec4(tokens + tb, n) : fold_tokens_scalar(tokens + tb, n);
+        int64_t h;
+        if (n == bs && x16_ok && tb + bs + 4 <= total_tok)
+          h = fold_tokens_x16(tokens, tb, bs);  // any alignment: 5 aligned LDG.128 / 16 tokens
+        else if (n == bs && ((bs & 3) == 0) && ((reinterpret_cast<uintptr_t>(tokens + tb) & 15) == 0))
+          h = fold_tokens_vec4(tokens + tb, n);
+        else
+          h = fold_tokens_scalar(tokens + tb, n);
+        keys[k0 + b] = h;
       }
     }
   }
