@@ -17,16 +17,24 @@
 //     (request, window) task per warp, lane = block, 128-bit token loads when
 //     aligned.  Contents are parked in keys[] (chain_hash results are >= 0;
 //     keys[] was pre-filled with -1 by block_hash_prep_kernel);
-//   * folding lanes (lane = request, claimed from a counter) on a few SMs
-//     reserved for them (by %smid) walk their request's keys[] 16 at a time
-//     with volatile loads, wait only on entries still -1, and overwrite each
-//     content with the chained key; producers join the folding when the
-//     content tasks run out.
+//   * folding lanes (lane = request, claimed from a counter) on SMs reserved
+//     for them by %smid -- one folding warp per SM sub-partition, because a
+//     lone chain runs at its ~97-cycle dependency latency while four per
+//     sub-partition are issue bound (tests/perf/hash_micro.cu) -- walk their
+//     request's keys[] 16 at a time: wait until the whole batch is produced
+//     (re-polled with one round of parallel volatile loads and exponential
+//     back-off -- tight polling measurably starves the producers of L2
+//     bandwidth), prefetch the next batch, chain, overwrite in place.
+//     Producers join the folding when the content tasks run out.
+// Measured on the Config 4 batch (4,096 requests, 4.17 M blocks): content
+// production alone 161 us; sequential produce-then-fold 373 us; this kernel
+// 237 us (tests/perf/hash_phase.py, KVX_HASH_FOLD_SMS sweeps the reserve).
 // Window-major production keeps every request's fold right behind its
 // producer, so the batch costs ~max(content throughput, longest fold) instead
 // of their sum.  Waiting happens only inside this single cooperative launch
 // (all CTAs co-resident), never between separate launches.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "kvx_common.cuh"
@@ -146,20 +154,30 @@ __device__ __forceinline__ void fold_requests(const int64_t* __restrict__ key_of
 #pragma unroll
     for (int j = 0; j < kFoldBatch; ++j) c[j] = (k0 + j < k1) ? ld_volatile(keys + k0 + j) : 0;
     for (int64_t k = k0; k < k1; k += kFoldBatch) {
-      int64_t nx[kFoldBatch];
+      const int m = static_cast<int>(min(static_cast<int64_t>(kFoldBatch), k1 - k));
+      // Wait for the whole batch, re-polling every missing entry in ONE round
+      // of parallel loads (polling them one by one would serialise an L2
+      // round trip per block whenever the fold catches up with production).
+      unsigned backoff = 512;  // ns; polling harder steals L2 bandwidth from the producers
+      while (true) {
+        bool ready = true;
+#pragma unroll
+        for (int j = 0; j < kFoldBatch; ++j) ready = ready && (j >= m || c[j] >= 0);
+        if (ready) break;
+        __nanosleep(backoff);
+        backoff = backoff < 4096 ? backoff * 2 : backoff;
+#pragma unroll
+        for (int j = 0; j < kFoldBatch; ++j)
+          if (j < m && c[j] < 0) c[j] = ld_volatile(keys + k + j);
+      }
+      int64_t nx[kFoldBatch];  // prefetch the next batch while this one is chained
 #pragma unroll
       for (int j = 0; j < kFoldBatch; ++j)
         nx[j] = (k + kFoldBatch + j < k1) ? ld_volatile(keys + k + kFoldBatch + j) : 0;
-      const int m = static_cast<int>(min(static_cast<int64_t>(kFoldBatch), k1 - k));
 #pragma unroll
       for (int j = 0; j < kFoldBatch; ++j) {
         if (j < m) {
-          int64_t v = c[j];
-          while (v < 0) {  // its producer has not reached this block yet
-            __nanosleep(32);
-            v = ld_volatile(keys + k + j);
-          }
-          prev = chain_hash(prev, static_cast<uint64_t>(v));
+          prev = chain_hash(prev, static_cast<uint64_t>(c[j]));
           keys[k + j] = prev;
         }
       }
@@ -221,7 +239,7 @@ __global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
       }
     }
   }
-  fold_requests(key_off, n_req, keys, ws);
+  if (fold_sms >= 0) fold_requests(key_off, n_req, keys, ws);
 }
 
 struct Workspace {
@@ -278,6 +296,7 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
   const int64_t lanes_per_fold_sm = static_cast<int64_t>(kFoldWarps) * 32;
   int fold_sms = static_cast<int>(std::min<int64_t>(
       std::max<int64_t>(1, (n_req + lanes_per_fold_sm - 1) / lanes_per_fold_sm), sms / 4));
+  if (const char* e = std::getenv("KVX_HASH_FOLD_SMS")) fold_sms = std::atoi(e);  // tuning/debug
   int bsi = static_cast<int>(bs);
   void* args[] = {const_cast<int32_t**>(&d_tokens), const_cast<int64_t**>(&d_tok_off), &n_req,
                   &bsi, const_cast<int64_t**>(&d_key_off), &d_keys, &ws, &fold_sms};

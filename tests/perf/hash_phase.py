@@ -1,0 +1,28 @@
+"""Time kvx_chain_hash_batch on the Config 4 batch (GPU).  With
+KVX_HASH_FOLD_SMS=-1 the kernel only produces content hashes (keys are then
+NOT final) -- used to split the stage-1a time into production and fold."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import paper_2407_00079_b200 as pkg  # noqa: E402
+from paper_2407_00079_b200.workloads import MatchWorkload  # noqa: E402
+
+mw = MatchWorkload().build()
+tokens = torch.as_tensor(mw.tokens, device="cuda")
+tok_off = torch.as_tensor(mw.tok_off, device="cuda")
+key_off = pkg.kvx.key_offsets(tok_off, 16)
+keys = torch.empty(int(key_off[-1].item()), dtype=torch.int64, device="cuda")
+for _ in range(3):
+    pkg.chain_hash_batch(tokens, tok_off, 16, key_off=key_off, keys=keys)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    pkg.chain_hash_batch(tokens, tok_off, 16, key_off=key_off, keys=keys)
+e1.record()
+torch.cuda.synchronize()
+print(f"fold_sms={os.environ.get('KVX_HASH_FOLD_SMS', 'auto')} "
+      f"hash batch: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
