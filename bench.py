@@ -53,6 +53,8 @@ def parse_args():
     ap.add_argument("--copy-impl", default="lsu", choices=["lsu", "tma"])
     ap.add_argument("--layers-per-chunk", type=int, default=1)
     ap.add_argument("--ring", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
+                    help="2: 64 x 8K requests, 50%% shared prefix (default); 3: one 128K request")
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--wave", type=int, default=16, help="decode wave (requests resident at once)")
     ap.add_argument("--block-size", type=int, default=16)
@@ -118,6 +120,38 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+class KernelTimer:
+    """CUDA-event pairs around launches on one stream (per-kernel roofline)."""
+
+    def __init__(self, enabled: bool = False):
+        self.enabled = enabled
+        self.pairs = []
+
+    def start(self, stream):
+        if not self.enabled:
+            return None
+        import torch
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def stop(self, stream, e0, nbytes: int):
+        if e0 is None:
+            return
+        import torch
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream)
+        self.pairs.append((e0, e1, nbytes))
+
+    def summary(self):
+        if not self.pairs:
+            return None
+        ms = [a.elapsed_time(b) for a, b, _ in self.pairs]
+        nbytes = [n for _, _, n in self.pairs]
+        return {"launches": len(ms), "avg_ms": sum(ms) / len(ms),
+                "avg_algorithmic_bytes": sum(nbytes) / len(nbytes)}
 
 
 def measured_peaks() -> dict:
@@ -241,6 +275,31 @@ def run_reference(args):
     return 0
 
 
+def build_plan(args, role):
+    """Block selections, pool shapes and per-pair units for --config 2 or 3."""
+    from paper_2407_00079_b200.workloads import LongContextWorkload, TransferWorkload
+    from paper_2407_00079_b200 import kvx
+    if args.config == 3:
+        wl = LongContextWorkload(block_size=args.block_size, dtype_bytes=args.dtype_bytes)
+        lo, hi = wl.layer_range(role.pair, role.pairs)
+        host_src = [wl.src_table]
+        host_dst = [wl.decode_table(kvx.SlotAllocator)] if role.role != "prefill" else None
+        return {"wl": wl, "host_src": host_src, "host_dst": host_dst,
+                "units": [(0, lo, hi, wl.chunk_blocks)], "max_blocks": wl.chunk_blocks,
+                "src_slots": wl.src_slots, "dst_slots": wl.dst_slots,
+                "payload_total": wl.payload_bytes(), "scaling": "strong",
+                "describe": wl.describe()}
+    wl = TransferWorkload(n_req=args.requests, wave=args.wave, block_size=args.block_size,
+                          dtype_bytes=args.dtype_bytes)
+    host_src = [wl.wave_src_table(w) for w in range(wl.n_waves)]
+    host_dst = wl.decode_tables(kvx.SlotAllocator) if role.role != "prefill" else None
+    return {"wl": wl, "host_src": host_src, "host_dst": host_dst,
+            "units": [(w, 0, wl.layers, 0) for w in range(wl.n_waves)],
+            "max_blocks": wl.wave * wl.blocks, "src_slots": wl.src_slots,
+            "dst_slots": wl.dst_slots, "payload_total": wl.payload_bytes() * role.pairs,
+            "scaling": "weak", "describe": wl.describe()}
+
+
 def run_kvx(args):
     import torch
     import torch.distributed as dist
@@ -249,9 +308,7 @@ def run_kvx(args):
     from paper_2407_00079_b200 import kvx
     from paper_2407_00079_b200.cluster import (exchange_with_peer, max_over_ranks,
                                                pair_topology, sum_over_ranks)
-    from paper_2407_00079_b200.streamer import (KernelTimer, LocalStream, PeerReceiver,
-                                                PeerSender)
-    from paper_2407_00079_b200.workloads import MatchWorkload, TransferWorkload
+    from paper_2407_00079_b200.streamer import NcclStreamer, Streamer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -264,6 +321,7 @@ def run_kvx(args):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     role = pair_topology(world, rank)
     kvx.set_copy_impl(args.copy_impl)
+    d = f"cuda:{dev}"
 
     def barrier():
         if world > 1:
@@ -275,117 +333,87 @@ def run_kvx(args):
     if (role.role == "local") != mode.startswith("local"):
         raise SystemExit(f"mode {mode} does not fit {world} GPU(s)")
 
-    wl = TransferWorkload(n_req=args.requests, wave=args.wave, block_size=args.block_size,
-                          dtype_bytes=args.dtype_bytes)
-    pool_kw = dict(layers=wl.layers, block_size=wl.block_size, heads=wl.heads,
-                   head_dim=wl.head_dim, dtype_bytes=wl.dtype_bytes)
-    max_blocks = wl.wave * wl.blocks
-    src = dst = None
-    if role.role in ("local", "prefill"):
-        src = pkg.KVPool(**pool_kw, slots=wl.src_slots, device=dev)
-        src.fill_synthetic(role.pair)
-    if role.role in ("local", "decode"):
-        dst = pkg.KVPool(**pool_kw, slots=wl.dst_slots, device=dev)
-        dst.tensor_view().zero_()
-
-    # decode block tables come from the decode instance's allocator
-    host_src = [wl.wave_src_table(w) for w in range(wl.n_waves)]
-    host_dst = wl.decode_tables(kvx.SlotAllocator) if dst is not None else None
-
-    if role.role == "local":
-        streamer = LocalStream(src, dst, mode, args.layers_per_chunk, args.ring, max_blocks)
-        streams = streamer.streams()
-        flags = kvx.DeviceBuffer(64, dev)
-        flags.tensor(torch.int64).zero_()
-    elif role.role == "prefill":
-        streamer = PeerSender(src, mode, args.layers_per_chunk, args.ring, max_blocks, role.peer)
-        peer = exchange_with_peer(role, streamer.export())
-        host_dst = peer["tables"]
-        streamer.connect(peer, {**pool_kw, "slots": wl.dst_slots})
-        streams = streamer.streams()
-    else:
-        streamer = PeerReceiver(dst, mode, args.layers_per_chunk, args.ring, max_blocks,
-                                role.peer)
-        exp = streamer.export()
-        exp["tables"] = host_dst
-        peer = exchange_with_peer(role, exp)
-        streamer.connect(peer)
-        streams = streamer.streams()
-
-    dev_src = [torch.as_tensor(t, device=f"cuda:{dev}") for t in host_src]
-    dev_dst = [torch.as_tensor(t, device=f"cuda:{dev}") for t in host_dst]
-    n_chunks = -(-wl.layers // args.layers_per_chunk)
     link_gbs = None
     if world > 1:
         g = probe_link(role, dev)
-        # slowest prefill -> decode link of the box (min over pairs)
-        link_gbs = -max_over_ranks(-(g if g is not None else 1e30), f"cuda:{dev}")
-    step_no = [0]
+        link_gbs = -max_over_ranks(-(g if g is not None else 1e30), d)  # slowest pair
 
-    def run_wave(w, timer):
-        if role.role == "local":
-            streamer.send_wave(dev_src[w], dev_dst[w], timer)
-        elif role.role == "prefill":
-            streamer.send_wave(dev_src[w], dev_dst[w], timer)
+    plan = build_plan(args, role)
+    wl = plan["wl"]
+    pool_kw = dict(layers=wl.layers, block_size=wl.block_size, heads=wl.heads,
+                   head_dim=wl.head_dim, dtype_bytes=wl.dtype_bytes)
+    slot_bytes = args.layers_per_chunk * 2 * plan["max_blocks"] * wl.slab_bytes
+    src = dst = None
+    if role.role in ("local", "prefill"):
+        src = pkg.KVPool(**pool_kw, slots=plan["src_slots"], device=dev)
+        src.fill_synthetic(role.pair)
+    if role.role in ("local", "decode"):
+        dst = pkg.KVPool(**pool_kw, slots=plan["dst_slots"], device=dev)
+        dst.tensor_view().zero_()
+
+    host_src, host_dst = plan["host_src"], plan["host_dst"]
+    if mode == "peer_nccl":
+        st = NcclStreamer("sender" if role.role == "prefill" else "receiver",
+                          src if src is not None else dst, role.peer, args.ring, slot_bytes)
+        peer = exchange_with_peer(role, {"tables": host_dst})
+        if role.role == "prefill":
+            host_dst = peer["tables"]
+    elif role.role == "local":
+        st = Streamer(mode, "local", src, dst, args.ring, slot_bytes)
+    else:
+        st = Streamer(mode, "sender" if role.role == "prefill" else "receiver", src, dst,
+                      args.ring, slot_bytes)
+        peer = exchange_with_peer(role, {"blob": st.export(), "tables": host_dst})
+        if role.role == "prefill":
+            host_dst = peer["tables"]
+            st.connect(peer["blob"], {**pool_kw, "slots": plan["dst_slots"]})
         else:
-            if mode == "peer_fused":
-                streamer.count_fused_chunks(n_chunks)
-            else:
-                streamer.recv_wave(dev_dst[w], dev_src[w].numel(), timer)
+            st.connect(peer["blob"])
+    main = st.stream
+    dev_src = [torch.as_tensor(t, device=d) for t in host_src]
+    dev_dst = [torch.as_tensor(np.asarray(t), device=d) for t in host_dst]
 
-    def end_step():
-        step_no[0] += 1
-        if role.role == "local":
-            # completion word of the step (read back by the e2e leg), ordered
-            # after the last scatter/copy of the step
-            join_streams(streams[0])
-            kvx.signal_write(flags.ptr, step_no[0], stream=streams[0])
+    def run_unit(u):
+        w, lo, hi, chunk = u
+        if role.role == "decode":
+            st.recv(dev_dst[w], lo, hi, chunk, args.layers_per_chunk)
         else:
-            streamer.end_step()
+            st.send(dev_src[w], dev_dst[w], lo, hi, chunk, args.layers_per_chunk)
 
-    def step(timer):
-        for w in range(wl.n_waves):
-            run_wave(w, timer)
-        end_step()
+    def step():
+        for u in plan["units"]:
+            run_unit(u)
+        st.finish()
 
-    def join_streams(main):
-        for s in streams:
-            if s is not main:
-                e = torch.cuda.Event()
-                e.record(s)
-                main.wait_event(e)
-
-    no_timer = KernelTimer(False)
     for _ in range(args.warmup):
-        step(no_timer)
+        step()
+    st.finish(main)
     torch.cuda.synchronize()
     barrier()
 
-    # ---- full-size parity property: every destination word of every wave
-    mismatch = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+    # ---- full-size parity: every destination word of every unit, each checked
+    # before the next unit reuses the same decode slots
+    mismatch = torch.zeros(1, dtype=torch.int64, device=d)
     checked = 0
-    for w in range(wl.n_waves):
-        run_wave(w, no_timer)
-        end_step()
-        for s in streams:
-            s.synchronize()
+    for u in plan["units"]:
+        run_unit(u)
+        st.finish(main)
+        main.synchronize()
         barrier()
         if dst is not None:
-            dst.verify(dev_dst[w], role.pair, dev_src[w], 0, wl.layers, counter=mismatch)
-            checked += dev_dst[w].numel() * wl.layers * 2 * wl.slab_bytes
-        # the next wave reuses the same decode slots: finish checking first
+            w, lo, hi, _ = u
+            dst.verify(dev_dst[w], role.pair, dev_src[w], lo, hi, counter=mismatch)
+            checked += dev_dst[w].numel() * (hi - lo) * 2 * wl.slab_bytes
         torch.cuda.synchronize()
         barrier()
-    torch.cuda.synchronize()
-    bad = int(sum_over_ranks(float(mismatch.item()), f"cuda:{dev}"))
-    checked = int(sum_over_ranks(float(checked), f"cuda:{dev}"))
+    bad = int(sum_over_ranks(float(mismatch.item()), d))
+    checked = int(sum_over_ranks(float(checked), d))
     if bad:
         raise SystemExit(f"PARITY FAILURE: {bad} mismatched 64-bit words")
-    barrier()
 
-    # ---- timed region (device events, max over ranks)
-    main = streams[0]
-    timer = KernelTimer(True)
+    # ---- timed region: CUDA events on the streamer's queue, max over ranks
+    st.set_timing(True)
+    st.launch_stats(reset=True)
     clocks = ClockSampler(dev)
     clocks.start()
     time.sleep(0.3)
@@ -394,74 +422,70 @@ def run_kvx(args):
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    for s in streams:
-        if s is not main:
-            s.wait_stream(main)
     e0.record(main)
-    for s in streams:
-        if s is not main:
-            s.wait_event(e0)
+    st.after(main)
     for _ in range(args.steps):
-        step(timer)
-    join_streams(main)
+        step()
+    st.finish(main)
     e1.record(main)
     torch.cuda.synchronize()
     barrier()
     launches = pkg.launch_count() - launches0
     clk = clocks.stop()
-    ms_total = max_over_ranks(e0.elapsed_time(e1), f"cuda:{dev}")
-    launches_all = int(sum_over_ranks(float(launches), f"cuda:{dev}"))
-    payload = wl.payload_bytes() * role.pairs
+    st.set_timing(False)
+    ksum = st.launch_stats(reset=True)
+    ms_total = max_over_ranks(e0.elapsed_time(e1), d)
+    launches_all = int(sum_over_ranks(float(launches), d))
+    payload = plan["payload_total"]
     value = payload * args.steps / (ms_total / 1e3) / GB
-    ksum = timer.summary()
-    ksum_all = {"avg_ms": max_over_ranks(ksum["avg_ms"] if ksum else 0.0, f"cuda:{dev}")}
+    kavg = max_over_ranks(ksum["avg_ms"] if ksum and ksum["launches"] else 0.0, d)
 
-    # ---- e2e: through the public API with HOST block tables every step
+    # ---- e2e: public API with HOST block tables every step (pinned H2D on the
+    # streamer queue), completion word D2H after the step
     e2e = None
     if not args.no_e2e:
         pin_src = [torch.as_tensor(t).pin_memory() for t in host_src]
         pin_dst = [torch.as_tensor(np.asarray(t)).pin_memory() for t in host_dst]
+        status_dev = torch.zeros(1, dtype=torch.int64, device=d)
         status = torch.zeros(1, dtype=torch.int64).pin_memory()
-        flag_t = (flags.tensor(torch.int64) if role.role == "local"
-                  else streamer.flags.tensor(torch.int64))
         h2d = sum(t.numel() * 4 for t in pin_src) + sum(t.numel() * 4 for t in pin_dst)
         torch.cuda.synchronize()
         barrier()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(main)
-        for s in streams:
-            if s is not main:
-                s.wait_event(f0)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             with torch.cuda.stream(main):
-                for w in range(wl.n_waves):
-                    dev_src[w].copy_(pin_src[w], non_blocking=True)
-                    dev_dst[w].copy_(pin_dst[w], non_blocking=True)
-            for s in streams:
-                if s is not main:
-                    s.wait_stream(main)
-            step(no_timer)
-            join_streams(main)
+                for a, b in zip(dev_src, pin_src):
+                    a.copy_(b, non_blocking=True)
+                for a, b in zip(dev_dst, pin_dst):
+                    a.copy_(b, non_blocking=True)
+            st.after(main)
+            step()
+            st.finish(main)
+            kvx.signal_write(status_dev.data_ptr(), i + 1, stream=main)
             with torch.cuda.stream(main):
-                status.copy_(flag_t[:1], non_blocking=True)
+                status.copy_(status_dev, non_blocking=True)
         f1.record(main)
         torch.cuda.synchronize()
         barrier()
-        e2e_ms = max_over_ranks(f0.elapsed_time(f1), f"cuda:{dev}")
+        assert int(status.item()) == args.steps
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1), d)
         e2e = {"value": payload * args.steps / (e2e_ms / 1e3) / GB, "unit": "GB/s",
-               "h2d_bytes_per_step": int(sum_over_ranks(float(h2d), f"cuda:{dev}")),
-               "d2h_bytes_per_step": int(sum_over_ranks(8.0, f"cuda:{dev}")),
-               "path": "python API -> libkvx C ABI; pinned host block tables H2D + completion "
-                       "word D2H inside the timed region; KV pools resident in HBM"}
+               "h2d_bytes_per_step": int(sum_over_ranks(float(h2d), d)),
+               "d2h_bytes_per_step": int(sum_over_ranks(8.0, d)),
+               "path": "python API -> libkvx C ABI (kvx_streamer_*); pinned host block tables "
+                       "H2D + completion word D2H inside the timed region; KV pools resident "
+                       "in HBM"}
 
-    # ---- secondary: prefix match (Config 4), every rank on its own replica
     match = None
     if not args.no_match:
         match = bench_match(args, dev, rank, world, role)
 
-    # release pool memory before the CPU leg
-    del streamer
+    st_close = getattr(st, "close", None)
+    if st_close:
+        st_close()
+    del src, dst
     torch.cuda.synchronize()
 
     cpu = None
@@ -470,22 +494,21 @@ def run_kvx(args):
 
     peaks = measured_peaks()
     roof = None
-    if ksum:
-        kname = {"local_fused": "copy_lsu_kernel", "local_staged": "copy_lsu_kernel",
-                 "peer_fused": "copy_lsu_kernel", "peer_ce": "copy_lsu_kernel",
-                 "peer_nccl": "copy_lsu_kernel"}[mode]
-        if args.copy_impl == "tma":
-            kname = "copy_tma_kernel"
-        achieved = ksum["avg_algorithmic_bytes"] / (ksum_all["avg_ms"] / 1e3) / GB
+    if ksum and ksum["launches"]:
+        kname = "copy_tma_kernel" if args.copy_impl == "tma" else "copy_lsu_kernel"
+        achieved = ksum["avg_algorithmic_bytes"] / (kavg / 1e3) / GB
         if mode == "peer_fused":
             bound, peak, pk_src = "nvlink", link_gbs, ("measured in this run: 1 GiB copy-engine "
                                                        "peer copy, slowest pair")
         else:
-            bound, peak, pk_src = "hbm", peaks["hbm_gbs"], f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"
-        tr = ncu_traffic(kname)
+            bound, peak = "hbm", peaks["hbm_gbs"]
+            pk_src = f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"
+        role_kernel = {"local_fused": "fused paged copy", "local_staged": "gather",
+                       "peer_ce": "gather (prefill GPU)", "peer_fused": "peer paged copy"}
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": tr, "kernel": kname,
-                "avg_launch_ms": ksum_all["avg_ms"], "launches_timed": ksum["launches"],
+                "frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname,
+                "launch_role": role_kernel.get(mode), "avg_launch_ms": kavg,
+                "launches_timed": ksum["launches"],
                 "algorithmic_bytes_per_launch": ksum["avg_algorithmic_bytes"],
                 "peak_source": pk_src}
 
@@ -495,13 +518,15 @@ def run_kvx(args):
                       "prefix-match blocks/s",
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "higher_is_better": True, "scaling": plan["scaling"], "vs_baseline": None,
+            "dtype": "u8",
             "data": "synthetic (counter-based splitmix64 KV content; generate_workload block ids)",
-            "config": {**wl.describe(), "mode": mode, "copy_impl": args.copy_impl,
-                       "layers_per_chunk": args.layers_per_chunk, "pairs": role.pairs,
+            "config": {**plan["describe"], "config": args.config, "mode": mode,
+                       "copy_impl": args.copy_impl, "layers_per_chunk": args.layers_per_chunk,
+                       "pairs": role.pairs,
                        "parallelism": ("local (prefill+decode on one GPU)" if world == 1 else
                                        f"{role.pairs}P->{role.pairs}D pairs"),
-                       "l2": "inputs larger than L2 (171.8 GB/pair/step); no flush needed"},
+                       "l2": "inputs far larger than L2 (126 MB); no flush needed"},
             "roofline": roof,
             "link": (None if world == 1 else {
                 "achieved_per_pair": value / role.pairs, "peak_per_direction": link_gbs,
@@ -560,7 +585,6 @@ def bench_match(args, dev, rank, world, role):
 
     import paper_2407_00079_b200 as pkg
     from paper_2407_00079_b200.cluster import max_over_ranks, sum_over_ranks
-    from paper_2407_00079_b200.streamer import KernelTimer
     from paper_2407_00079_b200.workloads import MatchWorkload
 
     mw = MatchWorkload().build()

@@ -147,6 +147,7 @@ int kvx_pool_destroy(kvx_pool* pool);
 void* kvx_pool_base(const kvx_pool* pool);
 int64_t kvx_pool_slab_bytes(const kvx_pool* pool);
 int64_t kvx_pool_bytes(const kvx_pool* pool);
+int kvx_pool_device(const kvx_pool* pool);
 
 /* Synthetic content: 64-bit word w of slab (pool_id, layer, kv, slot) =
  * mix64(slab_seed + w) (oracle/kvx_oracle.c). */
@@ -195,6 +196,59 @@ int kvx_transfer_query(kvx_xfer* x, uint64_t ticket);
 /* Queue a 64-bit flag store of `value` to d_flag (local or peer) on the
  * transfer queue, ordered after every copy submitted before it. */
 int kvx_transfer_signal(kvx_xfer* x, void* d_flag, uint64_t value);
+
+/* ---- layer-wise prefill -> decode stream (stages 2 -> 3 -> 4) ---------- */
+
+/* Host C++ engine sequencing the kernels and copy engines above: one request
+ * (or decode wave) is streamed as units of (block range, layer range), chunk-
+ * major, the way chunked-pipeline prefill produces KV (perf_model.cpp:87-110,
+ * sim_engine.cpp:455-470).  Ranks of a pair exchange kvx_streamer_export()
+ * blobs (CUDA IPC handles) and kvx_streamer_connect() to each other. */
+enum {
+  KVX_STREAM_LOCAL_FUSED = 0,  /* one GPU: paged -> paged copy kernel */
+  KVX_STREAM_LOCAL_STAGED = 1, /* one GPU: gather -> ring -> scatter */
+  KVX_STREAM_PEER_FUSED = 2,   /* sender kernel stores into the receiver's pool */
+  KVX_STREAM_PEER_CE = 3       /* gather -> copy engine P2P -> scatter on the receiver */
+};
+enum { KVX_ROLE_LOCAL = 0, KVX_ROLE_SENDER = 1, KVX_ROLE_RECEIVER = 2 };
+
+typedef struct {
+  int32_t mode;
+  int32_t role;
+  int32_t ring;           /* staging slots (staged modes) */
+  int32_t time_launches;  /* record CUDA events around each dominant launch */
+  int64_t slot_bytes;     /* bytes per staging slot (>= the largest unit) */
+} kvx_streamer_desc;
+
+typedef struct kvx_streamer kvx_streamer;
+
+int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* dst,
+                        kvx_streamer** out);
+int kvx_streamer_destroy(kvx_streamer* s);
+/* blob == NULL: *len = bytes needed. */
+int kvx_streamer_export(kvx_streamer* s, uint8_t* blob, int64_t cap, int64_t* len);
+/* peer_pool: the receiver's pool shape (PEER_FUSED sender only). */
+int kvx_streamer_connect(kvx_streamer* s, const uint8_t* blob, int64_t len,
+                         const kvx_pool_desc* peer_pool);
+void* kvx_streamer_stream(kvx_streamer* s);
+/* Sender / local: enqueue n blocks (device tables; dst table unused by PEER_CE
+ * senders) in units of chunk_blocks x layers_per_chunk. */
+int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t* d_dst_table,
+                      int64_t n, int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
+                      int32_t layers_per_chunk);
+/* Receiver: the matching units (same n / chunking / layer ranges). */
+int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_dst_table, int64_t n,
+                      int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
+                      int32_t layers_per_chunk);
+/* End of a step; if stream != NULL it then waits for all queued work. */
+int kvx_streamer_finish(kvx_streamer* s, void* stream);
+/* The streamer's queues wait for work already queued on stream. */
+int kvx_streamer_after(kvx_streamer* s, void* stream);
+int kvx_streamer_set_timing(kvx_streamer* s, int on);
+/* Host-blocking: timed dominant launches since the last reset. */
+int kvx_streamer_launch_stats(kvx_streamer* s, int64_t* launches, double* avg_ms,
+                              double* avg_bytes, int reset);
+uint64_t kvx_streamer_units(const kvx_streamer* s);
 
 /* ---- decode block table: deterministic slot allocator (host) ---------- */
 

@@ -1,0 +1,443 @@
+// kvx_stream.cpp -- the layer-wise prefill -> decode KV stream (stages 2->3->4)
+// as a host C++ engine over libkvx's kernels and copy engines.
+//
+// Reference behaviour it makes real:
+//   * the stream of a finished prefill: whole request chain, layer-wise,
+//     overlapping the prefill (proj/src/sim_engine.cpp:455-470; the paper's
+//     launch/wait per layer);
+//   * chunked pipeline prefill produces KV chunk by chunk (prefill_chunk =
+//     2048 tokens, proj/src/config.cpp:219; perf_model.cpp:87-110), so a long
+//     request streams (token chunk, layer range) units in chunk-major order;
+//   * one in-order transfer queue per sender (sender_busy_until_ms,
+//     proj/src/sim_engine.cpp:409-411).
+// A unit = (block range of the request, layer range).  Modes:
+//   LOCAL_FUSED   one GPU: paged->paged copy kernel per unit
+//   LOCAL_STAGED  one GPU: gather -> ring slot -> scatter (two streams)
+//   PEER_FUSED    sender kernel stores straight into the receiver's pool (IPC view)
+//   PEER_CE       sender gathers into a ring slot, the copy engine moves it into
+//                 the receiver's ring (IPC), the receiver scatters; 64-bit flags
+//                 written with stream memory operations order the three queues
+//                 across processes (no kernel ever spins on another's flag).
+// Sequence numbers only grow, so flags never need resetting (no ABA).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kvx.h"
+#include "kvx_common.cuh"
+
+using kvx::as_stream;
+using kvx::set_error;
+
+struct kvx_streamer {
+  kvx_streamer_desc d{};
+  kvx_pool* src = nullptr;
+  kvx_pool* dst = nullptr;
+  int device = 0;
+  cudaStream_t s_main = nullptr;     // gather / fused copy (sender, local) or scatter (receiver)
+  cudaStream_t s_second = nullptr;   // LOCAL_STAGED scatter stream
+  kvx_xfer* xfer = nullptr;          // PEER_CE copy queue
+  std::vector<void*> ring;           // local staging slots (cudaMalloc, IPC-exportable)
+  std::vector<void*> peer_ring;      // receiver's slots as mapped on the sender
+  std::vector<uint64_t> slot_ticket; // PEER_CE: copy that last read each gather slot
+  std::vector<cudaEvent_t> slot_ev;  // LOCAL_STAGED: scatter that last read each slot
+  std::vector<cudaEvent_t> gather_ev;
+  uint64_t* flag = nullptr;          // local 64-bit flag word (peer writes it)
+  uint64_t* peer_flag = nullptr;     // the peer's flag word, mapped here
+  kvx_pool* peer_view = nullptr;     // PEER_FUSED: receiver's pool as seen by the sender
+  uint64_t seq = 0;                  // units issued (sender) / consumed (receiver)
+  // optional per-launch timing of the dominant kernel
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
+  std::vector<double> timed_bytes;
+  size_t timed_used = 0;
+};
+
+namespace {
+
+int ev_pair(kvx_streamer* s, cudaEvent_t* a, cudaEvent_t* b) {
+  if (s->timed_used == s->timed.size()) {
+    cudaEvent_t x, y;
+    KVX_CUDA(cudaEventCreate(&x));
+    KVX_CUDA(cudaEventCreate(&y));
+    s->timed.push_back({x, y});
+    s->timed_bytes.push_back(0);
+  }
+  *a = s->timed[s->timed_used].first;
+  *b = s->timed[s->timed_used].second;
+  return KVX_OK;
+}
+
+// Wrap one dominant launch with timing events when enabled.
+template <class F>
+int timed_launch(kvx_streamer* s, cudaStream_t st, double bytes, F&& launch) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (s->timing) {
+    int rc = ev_pair(s, &a, &b);
+    if (rc) return rc;
+    KVX_CUDA(cudaEventRecord(a, st));
+  }
+  int rc = launch();
+  if (rc) return rc;
+  if (s->timing) {
+    KVX_CUDA(cudaEventRecord(b, st));
+    s->timed_bytes[s->timed_used] = bytes;
+    ++s->timed_used;
+  }
+  return KVX_OK;
+}
+
+bool is_peer(const kvx_streamer* s) {
+  return s->d.mode == KVX_STREAM_PEER_FUSED || s->d.mode == KVX_STREAM_PEER_CE;
+}
+
+struct ExportBlob {
+  int32_t magic;
+  int32_t mode;
+  int32_t ring;
+  int32_t has_pool;
+  int64_t slot_bytes;
+  uint8_t flag[KVX_IPC_HANDLE_BYTES];
+  uint8_t pool[KVX_IPC_HANDLE_BYTES];
+  // followed by ring * KVX_IPC_HANDLE_BYTES slot handles
+};
+constexpr int32_t kMagic = 0x6b767873;  // "kvxs"
+
+}  // namespace
+
+extern "C" {
+
+int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* dst,
+                        kvx_streamer** out) {
+  KVX_REQUIRE(desc && out, "kvx_streamer_create: NULL argument");
+  const int mode = desc->mode, role = desc->role;
+  KVX_REQUIRE(mode >= KVX_STREAM_LOCAL_FUSED && mode <= KVX_STREAM_PEER_CE,
+              "kvx_streamer_create: bad mode");
+  const bool local = mode == KVX_STREAM_LOCAL_FUSED || mode == KVX_STREAM_LOCAL_STAGED;
+  KVX_REQUIRE(local == (role == KVX_ROLE_LOCAL), "kvx_streamer_create: mode/role mismatch");
+  KVX_REQUIRE(role != KVX_ROLE_LOCAL || (src && dst), "local streamer needs src and dst pools");
+  KVX_REQUIRE(role != KVX_ROLE_SENDER || src, "sender needs a src pool");
+  KVX_REQUIRE(role != KVX_ROLE_RECEIVER || dst, "receiver needs a dst pool");
+  const bool staged = mode == KVX_STREAM_LOCAL_STAGED || mode == KVX_STREAM_PEER_CE;
+  KVX_REQUIRE(!staged || (desc->ring >= 1 && desc->slot_bytes > 0),
+              "staged modes need ring >= 1 and slot_bytes > 0");
+  auto* s = new kvx_streamer();
+  s->d = *desc;
+  s->src = src;
+  s->dst = dst;
+  s->device = src ? kvx_pool_device(src) : kvx_pool_device(dst);
+  s->timing = desc->time_launches != 0;
+  kvx::DeviceGuard g(s->device);
+  auto fail = [&](int rc) {
+    kvx_streamer_destroy(s);
+    return rc;
+  };
+  cudaError_t e = cudaStreamCreateWithFlags(&s->s_main, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: stream"));
+  if (mode == KVX_STREAM_LOCAL_STAGED) {
+    e = cudaStreamCreateWithFlags(&s->s_second, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: stream"));
+  }
+  if (staged) {
+    for (int i = 0; i < desc->ring; ++i) {
+      void* p = nullptr;
+      e = cudaMalloc(&p, static_cast<size_t>(desc->slot_bytes));
+      if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: ring"));
+      s->ring.push_back(p);
+      cudaEvent_t ev1, ev2;
+      cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming);
+      s->slot_ev.push_back(ev1);
+      s->gather_ev.push_back(ev2);
+    }
+    s->slot_ticket.assign(desc->ring, 0);
+  }
+  if (is_peer(s)) {
+    e = cudaMalloc(reinterpret_cast<void**>(&s->flag), 256);
+    if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: flag"));
+    cudaMemset(s->flag, 0, 256);
+    cudaDeviceSynchronize();
+  }
+  if (mode == KVX_STREAM_PEER_CE && role == KVX_ROLE_SENDER) {
+    int rc = kvx_xfer_create(s->device, &s->xfer);
+    if (rc) return fail(rc);
+  }
+  *out = s;
+  return KVX_OK;
+}
+
+int kvx_streamer_destroy(kvx_streamer* s) {
+  if (!s) return KVX_OK;
+  kvx::DeviceGuard g(s->device);
+  if (s->s_main) cudaStreamSynchronize(s->s_main);
+  if (s->s_second) cudaStreamSynchronize(s->s_second);
+  if (s->xfer) kvx_xfer_destroy(s->xfer);
+  for (void* p : s->peer_ring) kvx_ipc_close(p);
+  if (s->peer_flag) kvx_ipc_close(s->peer_flag);
+  if (s->peer_view) {
+    void* base = kvx_pool_base(s->peer_view);
+    kvx_pool_destroy(s->peer_view);
+    kvx_ipc_close(base);
+  }
+  for (void* p : s->ring) cudaFree(p);
+  for (auto ev : s->slot_ev) cudaEventDestroy(ev);
+  for (auto ev : s->gather_ev) cudaEventDestroy(ev);
+  for (auto& pr : s->timed) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  if (s->flag) cudaFree(s->flag);
+  if (s->s_main) cudaStreamDestroy(s->s_main);
+  if (s->s_second) cudaStreamDestroy(s->s_second);
+  delete s;
+  return KVX_OK;
+}
+
+int kvx_streamer_export(kvx_streamer* s, uint8_t* blob, int64_t cap, int64_t* len) {
+  KVX_REQUIRE(s && len, "kvx_streamer_export: NULL argument");
+  KVX_REQUIRE(is_peer(s), "kvx_streamer_export: only peer streamers export");
+  const int64_t need = static_cast<int64_t>(sizeof(ExportBlob)) +
+                       static_cast<int64_t>(s->ring.size()) * KVX_IPC_HANDLE_BYTES;
+  *len = need;
+  if (!blob) return KVX_OK;
+  KVX_REQUIRE(cap >= need, "kvx_streamer_export: blob too small");
+  ExportBlob b{};
+  b.magic = kMagic;
+  b.mode = s->d.mode;
+  b.ring = static_cast<int32_t>(s->ring.size());
+  b.slot_bytes = s->d.slot_bytes;
+  int rc = kvx_ipc_export(s->flag, b.flag);
+  if (rc) return rc;
+  if (s->d.role == KVX_ROLE_RECEIVER && s->d.mode == KVX_STREAM_PEER_FUSED) {
+    rc = kvx_ipc_export(kvx_pool_base(s->dst), b.pool);
+    if (rc) return rc;
+    b.has_pool = 1;
+  }
+  std::memcpy(blob, &b, sizeof(b));
+  for (size_t i = 0; i < s->ring.size(); ++i) {
+    rc = kvx_ipc_export(s->ring[i], blob + sizeof(b) + i * KVX_IPC_HANDLE_BYTES);
+    if (rc) return rc;
+  }
+  return KVX_OK;
+}
+
+int kvx_streamer_connect(kvx_streamer* s, const uint8_t* blob, int64_t len,
+                         const kvx_pool_desc* peer_pool) {
+  KVX_REQUIRE(s && blob && len >= static_cast<int64_t>(sizeof(ExportBlob)),
+              "kvx_streamer_connect: bad blob");
+  ExportBlob b;
+  std::memcpy(&b, blob, sizeof(b));
+  KVX_REQUIRE(b.magic == kMagic && b.mode == s->d.mode, "kvx_streamer_connect: peer mismatch");
+  kvx::DeviceGuard g(s->device);
+  void* p = nullptr;
+  int rc = kvx_ipc_open(b.flag, s->device, &p);
+  if (rc) return rc;
+  s->peer_flag = static_cast<uint64_t*>(p);
+  if (s->d.role == KVX_ROLE_SENDER && s->d.mode == KVX_STREAM_PEER_FUSED) {
+    KVX_REQUIRE(b.has_pool && peer_pool, "kvx_streamer_connect: peer pool missing");
+    rc = kvx_ipc_open(b.pool, s->device, &p);
+    if (rc) return rc;
+    kvx_pool_desc d = *peer_pool;
+    d.device = s->device;
+    rc = kvx_pool_create_view(&d, p, &s->peer_view);
+    if (rc) return rc;
+  }
+  if (s->d.role == KVX_ROLE_SENDER && s->d.mode == KVX_STREAM_PEER_CE) {
+    KVX_REQUIRE(b.ring == static_cast<int32_t>(s->ring.size()) && b.slot_bytes == s->d.slot_bytes,
+                "kvx_streamer_connect: ring shapes differ");
+    KVX_REQUIRE(len >= static_cast<int64_t>(sizeof(b)) + b.ring * KVX_IPC_HANDLE_BYTES,
+                "kvx_streamer_connect: truncated blob");
+    for (int i = 0; i < b.ring; ++i) {
+      rc = kvx_ipc_open(blob + sizeof(b) + i * KVX_IPC_HANDLE_BYTES, s->device, &p);
+      if (rc) return rc;
+      s->peer_ring.push_back(p);
+    }
+  }
+  return KVX_OK;
+}
+
+void* kvx_streamer_stream(kvx_streamer* s) { return s ? reinterpret_cast<void*>(s->s_main) : nullptr; }
+
+// Enqueue the units of one block range: chunk-major over [0, n) in
+// chunk_blocks, layer ranges of layers_per_chunk inside [layer_lo, layer_hi).
+int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t* d_dst_table,
+                      int64_t n, int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
+                      int32_t layers_per_chunk) {
+  KVX_REQUIRE(s && s->d.role != KVX_ROLE_RECEIVER, "kvx_streamer_send: not a sender");
+  KVX_REQUIRE(n >= 0 && chunk_blocks >= 1 && layers_per_chunk >= 1 && layer_lo <= layer_hi,
+              "kvx_streamer_send: bad ranges");
+  const bool needs_dst = s->d.mode != KVX_STREAM_PEER_CE;
+  KVX_REQUIRE(d_src_table && (!needs_dst || d_dst_table), "kvx_streamer_send: NULL table");
+  kvx::DeviceGuard g(s->device);
+  const int64_t slab = kvx_pool_slab_bytes(s->src);
+  const int R = static_cast<int>(s->ring.size());
+  for (int64_t b0 = 0; b0 < n; b0 += chunk_blocks) {
+    const int64_t nb = std::min(chunk_blocks, n - b0);
+    for (int32_t l0 = layer_lo; l0 < layer_hi; l0 += layers_per_chunk) {
+      const int32_t l1 = std::min(layer_hi, l0 + layers_per_chunk);
+      const int64_t payload = static_cast<int64_t>(l1 - l0) * 2 * nb * slab;
+      const uint64_t c = s->seq++;
+      int rc = KVX_OK;
+      switch (s->d.mode) {
+        case KVX_STREAM_LOCAL_FUSED:
+          rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
+            return kvx_copy_paged(s->src, d_src_table + b0, s->dst, d_dst_table + b0, nb, l0, l1,
+                                  s->s_main);
+          });
+          break;
+        case KVX_STREAM_PEER_FUSED:
+          KVX_REQUIRE(s->peer_view, "kvx_streamer_send: not connected");
+          rc = timed_launch(s, s->s_main, 1.0 * payload, [&] {
+            return kvx_copy_paged(s->src, d_src_table + b0, s->peer_view, d_dst_table + b0, nb,
+                                  l0, l1, s->s_main);
+          });
+          break;
+        case KVX_STREAM_LOCAL_STAGED: {
+          KVX_REQUIRE(payload <= s->d.slot_bytes, "kvx_streamer_send: unit larger than a slot");
+          const int slot = static_cast<int>(c % R);
+          if (c >= static_cast<uint64_t>(R)) KVX_CUDA(cudaStreamWaitEvent(s->s_main, s->slot_ev[slot], 0));
+          rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
+            return kvx_gather(s->src, d_src_table + b0, nb, l0, l1, s->ring[slot], s->s_main);
+          });
+          if (rc) return rc;
+          KVX_CUDA(cudaEventRecord(s->gather_ev[slot], s->s_main));
+          KVX_CUDA(cudaStreamWaitEvent(s->s_second, s->gather_ev[slot], 0));
+          rc = kvx_scatter(s->dst, d_dst_table + b0, nb, l0, l1, s->ring[slot], s->s_second);
+          if (rc) return rc;
+          KVX_CUDA(cudaEventRecord(s->slot_ev[slot], s->s_second));
+          break;
+        }
+        case KVX_STREAM_PEER_CE: {
+          KVX_REQUIRE(!s->peer_ring.empty(), "kvx_streamer_send: not connected");
+          KVX_REQUIRE(payload <= s->d.slot_bytes, "kvx_streamer_send: unit larger than a slot");
+          const int slot = static_cast<int>(c % R);
+          if (s->slot_ticket[slot]) {  // the copy that last read this gather slot
+            rc = kvx_transfer_wait_stream(s->xfer, s->slot_ticket[slot], s->s_main);
+            if (rc) return rc;
+          }
+          rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
+            return kvx_gather(s->src, d_src_table + b0, nb, l0, l1, s->ring[slot], s->s_main);
+          });
+          if (rc) return rc;
+          if (c >= static_cast<uint64_t>(R)) {  // receiver drained its slot (unit c - R)
+            rc = kvx_signal_wait(kvx_xfer_stream(s->xfer), s->flag, c - R + 1);
+            if (rc) return rc;
+          }
+          rc = kvx_transfer_submit(s->xfer, s->peer_ring[slot], s->ring[slot], payload, s->s_main,
+                                   &s->slot_ticket[slot]);
+          if (rc) return rc;
+          rc = kvx_transfer_signal(s->xfer, s->peer_flag, c + 1);  // unit c landed
+          break;
+        }
+        default:
+          return set_error(KVX_EINVAL, "kvx_streamer_send: bad mode");
+      }
+      if (rc) return rc;
+    }
+  }
+  return KVX_OK;
+}
+
+int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_dst_table, int64_t n,
+                      int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
+                      int32_t layers_per_chunk) {
+  KVX_REQUIRE(s && s->d.role == KVX_ROLE_RECEIVER, "kvx_streamer_recv: not a receiver");
+  KVX_REQUIRE(n >= 0 && chunk_blocks >= 1 && layers_per_chunk >= 1 && layer_lo <= layer_hi,
+              "kvx_streamer_recv: bad ranges");
+  kvx::DeviceGuard g(s->device);
+  const int64_t slab = kvx_pool_slab_bytes(s->dst);
+  const int R = static_cast<int>(s->ring.size());
+  for (int64_t b0 = 0; b0 < n; b0 += chunk_blocks) {
+    const int64_t nb = std::min(chunk_blocks, n - b0);
+    for (int32_t l0 = layer_lo; l0 < layer_hi; l0 += layers_per_chunk) {
+      const int32_t l1 = std::min(layer_hi, l0 + layers_per_chunk);
+      const int64_t payload = static_cast<int64_t>(l1 - l0) * 2 * nb * slab;
+      const uint64_t c = s->seq++;
+      if (s->d.mode != KVX_STREAM_PEER_CE) continue;  // PEER_FUSED: bytes land without us
+      KVX_REQUIRE(d_dst_table, "kvx_streamer_recv: NULL table");
+      const int slot = static_cast<int>(c % R);
+      int rc = kvx_signal_wait(s->s_main, s->flag, c + 1);
+      if (rc) return rc;
+      rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
+        return kvx_scatter(s->dst, d_dst_table + b0, nb, l0, l1, s->ring[slot], s->s_main);
+      });
+      if (rc) return rc;
+      rc = kvx_signal_write(s->s_main, s->peer_flag, c + 1);  // slot drained
+      if (rc) return rc;
+    }
+  }
+  return KVX_OK;
+}
+
+// Close a step: PEER_FUSED sender publishes its unit count; the receiver's
+// stream waits for it.  Then `stream` (if given) waits for all queued work.
+int kvx_streamer_finish(kvx_streamer* s, void* stream) {
+  KVX_REQUIRE(s != nullptr, "kvx_streamer_finish: NULL");
+  kvx::DeviceGuard g(s->device);
+  if (s->d.mode == KVX_STREAM_PEER_FUSED) {
+    int rc = s->d.role == KVX_ROLE_SENDER ? kvx_signal_write(s->s_main, s->peer_flag, s->seq)
+                                          : kvx_signal_wait(s->s_main, s->flag, s->seq);
+    if (rc) return rc;
+  }
+  if (stream) {
+    cudaEvent_t ev;
+    KVX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    std::vector<cudaStream_t> qs = {s->s_main};
+    if (s->s_second) qs.push_back(s->s_second);
+    if (s->xfer) qs.push_back(as_stream(kvx_xfer_stream(s->xfer)));
+    for (cudaStream_t q : qs) {
+      KVX_CUDA(cudaEventRecord(ev, q));
+      KVX_CUDA(cudaStreamWaitEvent(as_stream(stream), ev, 0));
+    }
+    KVX_CUDA(cudaEventDestroy(ev));
+  }
+  return KVX_OK;
+}
+
+// Make the streamer's queues wait for work already queued on `stream`.
+int kvx_streamer_after(kvx_streamer* s, void* stream) {
+  KVX_REQUIRE(s != nullptr, "kvx_streamer_after: NULL");
+  kvx::DeviceGuard g(s->device);
+  cudaEvent_t ev;
+  KVX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  KVX_CUDA(cudaEventRecord(ev, as_stream(stream)));
+  KVX_CUDA(cudaStreamWaitEvent(s->s_main, ev, 0));
+  if (s->s_second) KVX_CUDA(cudaStreamWaitEvent(s->s_second, ev, 0));
+  if (s->xfer) KVX_CUDA(cudaStreamWaitEvent(as_stream(kvx_xfer_stream(s->xfer)), ev, 0));
+  KVX_CUDA(cudaEventDestroy(ev));
+  return KVX_OK;
+}
+
+// Host-blocking: average duration and algorithmic bytes of the timed launches
+// since the last reset.
+int kvx_streamer_launch_stats(kvx_streamer* s, int64_t* launches, double* avg_ms,
+                              double* avg_bytes, int reset) {
+  KVX_REQUIRE(s && launches && avg_ms && avg_bytes, "kvx_streamer_launch_stats: NULL");
+  kvx::DeviceGuard g(s->device);
+  double ms_sum = 0, bytes_sum = 0;
+  for (size_t i = 0; i < s->timed_used; ++i) {
+    KVX_CUDA(cudaEventSynchronize(s->timed[i].second));
+    float ms = 0;
+    KVX_CUDA(cudaEventElapsedTime(&ms, s->timed[i].first, s->timed[i].second));
+    ms_sum += ms;
+    bytes_sum += s->timed_bytes[i];
+  }
+  *launches = static_cast<int64_t>(s->timed_used);
+  *avg_ms = s->timed_used ? ms_sum / s->timed_used : 0.0;
+  *avg_bytes = s->timed_used ? bytes_sum / s->timed_used : 0.0;
+  if (reset) s->timed_used = 0;
+  return KVX_OK;
+}
+
+int kvx_streamer_set_timing(kvx_streamer* s, int on) {
+  KVX_REQUIRE(s != nullptr, "kvx_streamer_set_timing: NULL");
+  s->timing = on != 0;
+  return KVX_OK;
+}
+
+uint64_t kvx_streamer_units(const kvx_streamer* s) { return s ? s->seq : 0; }
+
+}  // extern "C"

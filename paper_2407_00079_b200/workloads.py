@@ -110,6 +110,57 @@ class TransferWorkload:
 
 
 @dataclass
+class LongContextWorkload:
+    """Config 3: one 128K-token request, streamed in 2,048-token chunks
+    (prefill_chunk, proj/src/config.cpp:219) layer by layer; with P pairs each
+    pair owns a contiguous layer range (a CPP stage = a layer range,
+    proj/tests/oracles.hpp:120-137), so total work is fixed (strong scaling)."""
+    tokens: int = 131072
+    block_size: int = 16
+    chunk_tokens: int = 2048
+    layers: int = 80
+    heads: int = 8
+    head_dim: int = 128
+    dtype_bytes: int = 2
+    decode_fragmentation: float = 0.2
+    seed: int = 3
+
+    def __post_init__(self):
+        self.blocks = -(-self.tokens // self.block_size)
+        rng = np.random.default_rng(self.seed)
+        self.src_slots = self.blocks
+        self.src_table = rng.permutation(self.src_slots).astype(np.int32)
+        self.dst_slots = int(np.ceil(self.blocks / (1.0 - self.decode_fragmentation)))
+        self.dst_preoccupied = np.sort(rng.choice(
+            self.dst_slots, size=self.dst_slots - self.blocks, replace=False)).astype(np.int32)
+        self.chunk_blocks = self.chunk_tokens // self.block_size
+
+    @property
+    def slab_bytes(self) -> int:
+        return self.block_size * self.heads * self.head_dim * self.dtype_bytes
+
+    def layer_range(self, pair: int, pairs: int):
+        return (pair * self.layers // pairs, (pair + 1) * self.layers // pairs)
+
+    def payload_bytes(self, pair: int = 0, pairs: int = 1) -> int:
+        lo, hi = self.layer_range(pair, pairs)
+        return self.blocks * (hi - lo) * 2 * self.slab_bytes
+
+    def decode_table(self, allocator_factory) -> np.ndarray:
+        alloc = allocator_factory(self.dst_slots)
+        alloc.mark(self.dst_preoccupied)
+        return np.array(alloc.take(self.blocks), copy=True)
+
+    def describe(self) -> dict:
+        return {"workload": "config3: 1 x 128K-token request, 2048-token chunks, layer-wise, "
+                            "layer-range shards per pair", "tokens": self.tokens,
+                "block_size": self.block_size, "chunk_tokens": self.chunk_tokens,
+                "layers": self.layers, "kv_heads": self.heads, "head_dim": self.head_dim,
+                "kv_dtype": {1: "fp8", 2: "fp16", 4: "fp32"}[self.dtype_bytes],
+                "payload_bytes_total": self.payload_bytes()}
+
+
+@dataclass
 class MatchWorkload:
     """Config 4: Kimi-like trace; N requests, lengths U[8K, 24K], Zipf(alpha)
     session choice over `sessions` sessions; each request reuses a prefix of

@@ -1,0 +1,83 @@
+"""GPU parity of the C++ layer-wise streamer (kvx_streamer_*): local modes on
+one GPU against the C restatement (memcmp), and -- when the box has 2+ GPUs --
+the peer modes through bench.py under torchrun (every destination word is
+verified inside bench.py; a mismatch exits non-zero)."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=torch.int32, device=DEV)
+
+
+@pytest.mark.parametrize("mode", ["local_fused", "local_staged"])
+@pytest.mark.parametrize("chunk,lpc", [(0, 1), (5, 1), (7, 3), (64, 80)])
+def test_local_streamer_vs_oracle(kvx, oracle_lib, mode, chunk, lpc):
+    from paper_2407_00079_b200.streamer import Streamer
+    L, bs, n = 6, 16, 23
+    src = kvx.KVPool(L, bs, 8, 128, 2, 40, 0)
+    dst = kvx.KVPool(L, bs, 8, 128, 2, 50, 0)
+    src.fill_synthetic(4)
+    dst.tensor_view().zero_()
+    rng = np.random.default_rng(chunk * 10 + lpc)
+    st_tab = rng.integers(0, 40, size=n).astype(np.int32)
+    dt_tab = rng.permutation(50)[:n].astype(np.int32)
+    cb = chunk or n
+    slot = min(lpc, L) * 2 * min(cb, n) * src.slab
+    s = Streamer(mode, "local", src, dst, ring=2, slot_bytes=slot)
+    s.send(_t(st_tab), _t(dt_tab), 1, L, chunk, lpc)
+    s.finish()
+    s.finish(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    want = np.zeros(dst.nbytes, dtype=np.uint8)
+    o = oracle_lib
+    o.copy_paged(src.tensor_view().cpu().numpy(), 40, st_tab, want, 50, dt_tab, src.slab, 1, L)
+    assert np.array_equal(dst.tensor_view().cpu().numpy(), want)
+    units = -(-n // cb) * -(-(L - 1) // lpc)
+    assert s.units == units
+
+
+def test_streamer_rejects_bad_shapes(kvx):
+    from paper_2407_00079_b200.streamer import Streamer
+    src = kvx.KVPool(2, 16, 8, 128, 2, 8, 0)
+    with pytest.raises(kvx.ValidationError):
+        Streamer("local_fused", "sender", src, None)
+    with pytest.raises(kvx.ValidationError):
+        Streamer("peer_ce", "sender", src, None, ring=0, slot_bytes=0)
+
+
+def _torchrun(n, *args, timeout=900):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", "bench.py", "--gpus", str(n),
+           *args]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
+    return json.loads(line)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+@pytest.mark.parametrize("mode", ["peer_ce", "peer_fused", "peer_nccl"])
+def test_two_gpu_modes_bit_exact(mode):
+    d = _torchrun(2, "--mode", mode, "--requests", "4", "--wave", "2", "--steps", "2",
+                  "--warmup", "3", "--no-match", "--no-e2e", "--no-cpu-baseline")
+    assert d["parity"]["mismatched_words"] == 0 and d["parity"]["checked_bytes"] > 0
+    assert d["value"] > 0 and d["link"]["peak_per_direction"] > 0
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_two_gpu_long_context_chunked():
+    d = _torchrun(2, "--config", "3", "--block-size", "64", "--steps", "2", "--warmup", "3",
+                  "--no-match", "--no-e2e", "--no-cpu-baseline")
+    assert d["parity"]["mismatched_words"] == 0 and d["scaling"] == "strong"
