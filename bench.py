@@ -369,7 +369,8 @@ def run_kvx(args):
             st.connect(peer["blob"], {**pool_kw, "slots": plan["dst_slots"]})
         else:
             st.connect(peer["blob"])
-    main = st.stream
+    main = torch.cuda.Stream(dev)  # torch-owned queue: H2D/D2H, timing events; the streamer
+    # queues are ordered against it with st.after(main) / st.finish(main)
     dev_src = [torch.as_tensor(t, device=d) for t in host_src]
     dev_dst = [torch.as_tensor(np.asarray(t), device=d) for t in host_dst]
 
@@ -385,6 +386,7 @@ def run_kvx(args):
             run_unit(u)
         st.finish()
 
+    st.after(main)
     for _ in range(args.warmup):
         step()
     st.finish(main)
@@ -396,6 +398,7 @@ def run_kvx(args):
     mismatch = torch.zeros(1, dtype=torch.int64, device=d)
     checked = 0
     for u in plan["units"]:
+        st.after(main)
         run_unit(u)
         st.finish(main)
         main.synchronize()
@@ -482,10 +485,6 @@ def run_kvx(args):
     if not args.no_match:
         match = bench_match(args, dev, rank, world, role)
 
-    st_close = getattr(st, "close", None)
-    if st_close:
-        st_close()
-    del src, dst
     torch.cuda.synchronize()
 
     cpu = None
