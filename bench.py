@@ -415,7 +415,9 @@ def run_kvx(args):
         raise SystemExit(f"PARITY FAILURE: {bad} mismatched 64-bit words")
 
     # ---- timed region: CUDA events on the streamer's queue, max over ranks
-    st.set_timing(True)
+    # time a sample of the dominant launches: every launch when units are large,
+    # every 16th when they are small (an event pair costs ~µs of host time)
+    st.set_timing(True, 1 if args.config == 2 else 16)
     st.launch_stats(reset=True)
     clocks = ClockSampler(dev)
     clocks.start()

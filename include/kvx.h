@@ -244,7 +244,8 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_dst_table, int64_t n,
 int kvx_streamer_finish(kvx_streamer* s, void* stream);
 /* The streamer's queues wait for work already queued on stream. */
 int kvx_streamer_after(kvx_streamer* s, void* stream);
-int kvx_streamer_set_timing(kvx_streamer* s, int on);
+/* Time every stride-th dominant launch with CUDA events (0/1 = off/on). */
+int kvx_streamer_set_timing(kvx_streamer* s, int on, int stride);
 /* Host-blocking: timed dominant launches since the last reset. */
 int kvx_streamer_launch_stats(kvx_streamer* s, int64_t* launches, double* avg_ms,
                               double* avg_bytes, int reset);

@@ -51,6 +51,8 @@ struct kvx_streamer {
   uint64_t seq = 0;                  // units issued (sender) / consumed (receiver)
   // optional per-launch timing of the dominant kernel
   bool timing = false;
+  uint64_t timing_stride = 1;  // time every stride-th dominant launch (event records cost host time)
+  uint64_t timing_count = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
   std::vector<double> timed_bytes;
   size_t timed_used = 0;
@@ -75,14 +77,15 @@ int ev_pair(kvx_streamer* s, cudaEvent_t* a, cudaEvent_t* b) {
 template <class F>
 int timed_launch(kvx_streamer* s, cudaStream_t st, double bytes, F&& launch) {
   cudaEvent_t a = nullptr, b = nullptr;
-  if (s->timing) {
+  const bool on = s->timing && (s->timing_count++ % s->timing_stride == 0);
+  if (on) {
     int rc = ev_pair(s, &a, &b);
     if (rc) return rc;
     KVX_CUDA(cudaEventRecord(a, st));
   }
   int rc = launch();
   if (rc) return rc;
-  if (s->timing) {
+  if (on) {
     KVX_CUDA(cudaEventRecord(b, st));
     s->timed_bytes[s->timed_used] = bytes;
     ++s->timed_used;
@@ -432,9 +435,11 @@ int kvx_streamer_launch_stats(kvx_streamer* s, int64_t* launches, double* avg_ms
   return KVX_OK;
 }
 
-int kvx_streamer_set_timing(kvx_streamer* s, int on) {
-  KVX_REQUIRE(s != nullptr, "kvx_streamer_set_timing: NULL");
+int kvx_streamer_set_timing(kvx_streamer* s, int on, int stride) {
+  KVX_REQUIRE(s != nullptr && stride >= 1, "kvx_streamer_set_timing: bad arguments");
   s->timing = on != 0;
+  s->timing_stride = static_cast<uint64_t>(stride);
+  s->timing_count = 0;
   return KVX_OK;
 }
 

@@ -47,7 +47,7 @@ _sig("kvx_streamer_send", C.c_int, _vp, _vp, _vp, _i64, _i64, C.c_int32, C.c_int
 _sig("kvx_streamer_recv", C.c_int, _vp, _vp, _i64, _i64, C.c_int32, C.c_int32, C.c_int32)
 _sig("kvx_streamer_finish", C.c_int, _vp, _vp)
 _sig("kvx_streamer_after", C.c_int, _vp, _vp)
-_sig("kvx_streamer_set_timing", C.c_int, _vp, C.c_int)
+_sig("kvx_streamer_set_timing", C.c_int, _vp, C.c_int, C.c_int)
 _sig("kvx_streamer_launch_stats", C.c_int, _vp, C.POINTER(_i64), C.POINTER(C.c_double),
      C.POINTER(C.c_double), C.c_int)
 _sig("kvx_streamer_units", C.c_uint64, _vp)
@@ -113,8 +113,8 @@ class Streamer:
     def after(self, stream):
         check(_L.kvx_streamer_after(self.h, kvx._stream(stream)))
 
-    def set_timing(self, on: bool):
-        check(_L.kvx_streamer_set_timing(self.h, int(on)))
+    def set_timing(self, on: bool, stride: int = 1):
+        check(_L.kvx_streamer_set_timing(self.h, int(on), stride))
 
     def launch_stats(self, reset: bool = True):
         n, ms, b = _i64(), C.c_double(), C.c_double()
@@ -186,7 +186,7 @@ class NcclStreamer:
         for q in (self.stream, self.comm):
             q.wait_stream(stream)
 
-    def set_timing(self, on):
+    def set_timing(self, on, stride=1):
         pass
 
     def launch_stats(self, reset=True):
