@@ -51,7 +51,10 @@ def parse_args():
                     choices=["auto", "local_fused", "local_staged", "peer_fused", "peer_ce",
                              "peer_nccl"])
     ap.add_argument("--copy-impl", default="lsu", choices=["lsu", "tma"])
-    ap.add_argument("--layers-per-chunk", type=int, default=1)
+    ap.add_argument("--layers-per-chunk", type=int, default=0,
+                    help="layers per streamed unit; 0 = auto (1 for config 2, whose units are "
+                         "512 MiB per layer; 16 for config 3, whose 2048-token chunks are only "
+                         "8 MiB per layer and launch-overhead bound one layer at a time)")
     ap.add_argument("--ring", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=[2, 3],
                     help="2: 64 x 8K requests, 50%% shared prefix (default); 3: one 128K request")
@@ -338,6 +341,8 @@ def run_kvx(args):
         g = probe_link(role, dev)
         link_gbs = -max_over_ranks(-(g if g is not None else 1e30), d)  # slowest pair
 
+    if args.layers_per_chunk <= 0:
+        args.layers_per_chunk = 1 if args.config == 2 else 16
     plan = build_plan(args, role)
     wl = plan["wl"]
     pool_kw = dict(layers=wl.layers, block_size=wl.block_size, heads=wl.heads,
