@@ -148,6 +148,7 @@ void* kvx_pool_base(const kvx_pool* pool);
 int64_t kvx_pool_slab_bytes(const kvx_pool* pool);
 int64_t kvx_pool_bytes(const kvx_pool* pool);
 int kvx_pool_device(const kvx_pool* pool);
+int32_t kvx_pool_layers(const kvx_pool* pool);
 
 /* Synthetic content: 64-bit word w of slab (pool_id, layer, kv, slot) =
  * mix64(slab_seed + w) (oracle/kvx_oracle.c). */
@@ -250,6 +251,29 @@ int kvx_streamer_set_timing(kvx_streamer* s, int on, int stride);
 int kvx_streamer_launch_stats(kvx_streamer* s, int64_t* launches, double* avg_ms,
                               double* avg_bytes, int reset);
 uint64_t kvx_streamer_units(const kvx_streamer* s);
+
+/* ---- KVCache store of one instance + migration (hot-spot replication) ---- */
+
+/* A store = paged pool + block index (key -> pool slot) + slot allocator.
+ * put: index new keys at the lowest free slots (existing keys keep theirs);
+ * get: slot per key or -1; evict: drop keys and free their slots.
+ * migrate: copy the KV of keys resident in src into dst (every layer, K and
+ * V), skipping keys dst already holds, and index them there -- the byte path
+ * behind the reference's migration events (sim_engine.cpp:399-419,605-650).
+ * If ANY key is not resident in src the call returns KVX_EABORTED and changes
+ * nothing (the reference aborts when the source evicted part of the range).
+ * All key/slot arrays are HOST arrays; calls are host-blocking. */
+typedef struct kvx_store kvx_store;
+int kvx_store_create(const kvx_pool_desc* desc, kvx_store** out);
+int kvx_store_destroy(kvx_store* s);
+kvx_pool* kvx_store_pool(kvx_store* s);
+kvx_index* kvx_store_index(kvx_store* s);
+void* kvx_store_stream(kvx_store* s);
+int kvx_store_put(kvx_store* s, const int64_t* keys, int64_t n, int32_t* slots_out);
+int kvx_store_get(kvx_store* s, const int64_t* keys, int64_t n, int32_t* slots_out);
+int kvx_store_evict(kvx_store* s, const int64_t* keys, int64_t n);
+int kvx_store_migrate(kvx_store* src, kvx_store* dst, const int64_t* keys, int64_t n,
+                      int64_t* n_copied);
 
 /* ---- decode block table: deterministic slot allocator (host) ---------- */
 

@@ -361,6 +361,7 @@ void* kvx_pool_base(const kvx_pool* p) { return p ? p->base : nullptr; }
 int64_t kvx_pool_slab_bytes(const kvx_pool* p) { return p ? p->slab : 0; }
 int64_t kvx_pool_bytes(const kvx_pool* p) { return p ? p->bytes : 0; }
 int kvx_pool_device(const kvx_pool* p) { return p ? p->d.device : -1; }
+int32_t kvx_pool_layers(const kvx_pool* p) { return p ? p->d.layers : 0; }
 
 int kvx_set_copy_impl(int impl) {
   KVX_REQUIRE(impl == 0 || impl == 1, "kvx_set_copy_impl: impl must be 0 (LSU) or 1 (TMA)");

@@ -295,7 +295,7 @@ class KVPool:
         self.base = int(_L.kvx_pool_base(h))
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and getattr(self, "owned", True):
             _L.kvx_pool_destroy(self.h)
             self.h = None
 
