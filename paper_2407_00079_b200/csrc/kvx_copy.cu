@@ -18,10 +18,11 @@
 //           32 KiB: all 128-bit loads (ld.global.nc.L1::no_allocate) are
 //           issued before any store, 4 per thread in flight.
 //   TMA  -- one elected thread per CTA drives cp.async.bulk global->shared
-//           (mbarrier complete_tx) and shared->global bulk stores through an
-//           8-stage shared-memory ring: 4 loads and up to 4 stores in flight
-//           per SM with no register staging.
+//           (mbarrier complete_tx) and shared->global bulk stores through a
+//           shared-memory ring (default 12 x 16 KiB stages, 8 loads in
+//           flight = 128 KiB per SM) with no register staging.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kvx_common.cuh"
 
@@ -92,10 +93,6 @@ __global__ void __launch_bounds__(kLsuThreads) copy_lsu_kernel(const SlabCopy c)
 }
 
 // ---- TMA bulk-copy pipeline ----------------------------------------------
-constexpr int kTmaStages = 8;
-constexpr int kTmaAhead = 4;                 // loads in flight
-constexpr int64_t kTmaStage = 16 * 1024;     // bytes per stage
-constexpr int kTmaSmem = kTmaStages * kTmaStage;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -148,14 +145,17 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+template <int STAGES, int AHEAD, int STAGE_BYTES>
 __global__ void __launch_bounds__(32) copy_tma_kernel(const SlabCopy c) {
+  static_assert(AHEAD < STAGES, "need a free stage beyond the loads in flight");
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[kTmaStages];
+  __shared__ __align__(8) uint64_t bars[STAGES];
   if (threadIdx.x != 0) return;
-  for (int s = 0; s < kTmaStages; ++s) mbar_init(&bars[s], 1);
+  for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 
-  const int64_t parts = (c.slab + kTmaStage - 1) / kTmaStage;
+  constexpr int64_t kStage = STAGE_BYTES;
+  const int64_t parts = (c.slab + kStage - 1) / kStage;
   const int64_t items = c.planes * c.n * parts;
   // this CTA's items: blockIdx.x, blockIdx.x + gridDim.x, ...
   const int64_t mine = items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -163,40 +163,58 @@ __global__ void __launch_bounds__(32) copy_tma_kernel(const SlabCopy c) {
   auto item_addr = [&](int64_t k, const uint8_t*& s, uint8_t*& d, uint32_t& bytes) {
     const int64_t it = blockIdx.x + k * gridDim.x;
     const int64_t u = it / parts;
-    const int64_t off = (it - u * parts) * kTmaStage;
+    const int64_t off = (it - u * parts) * kStage;
     unit_addrs(c, u, s, d);
     s += off;
     d += off;
-    bytes = static_cast<uint32_t>(min(kTmaStage, c.slab - off));
+    bytes = static_cast<uint32_t>(min(kStage, c.slab - off));
   };
 
-  for (int64_t k = 0; k < mine + kTmaAhead; ++k) {
-    // consume item k - kTmaAhead: its load has landed -> bulk store it out
-    const int64_t kc = k - kTmaAhead;
+  for (int64_t k = 0; k < mine + AHEAD; ++k) {
+    // consume item k - AHEAD: its load has landed -> bulk store it out
+    const int64_t kc = k - AHEAD;
     if (kc >= 0) {
-      const int st = static_cast<int>(kc % kTmaStages);
-      mbar_wait(&bars[st], static_cast<uint32_t>((kc / kTmaStages) & 1));
+      const int st = static_cast<int>(kc % STAGES);
+      mbar_wait(&bars[st], static_cast<uint32_t>((kc / STAGES) & 1));
       const uint8_t* s;
       uint8_t* d;
       uint32_t bytes;
       item_addr(kc, s, d, bytes);
-      bulk_store(d, smem + st * kTmaStage, bytes);
+      bulk_store(d, smem + st * kStage, bytes);
     }
-    // produce item k into its stage once the store that last used it has
-    // finished reading shared memory (stores committed: items <= kc; the
-    // stage's previous user is item k - kTmaStages).
+    // produce item k into its stage once the store that last used it (item
+    // k - STAGES; stores committed so far: items <= kc) has read shared memory
     if (k < mine) {
-      if (k >= kTmaStages) bulk_wait_read<kTmaStages - kTmaAhead>();
-      const int st = static_cast<int>(k % kTmaStages);
+      if (k >= STAGES) bulk_wait_read<STAGES - AHEAD>();
+      const int st = static_cast<int>(k % STAGES);
       const uint8_t* s;
       uint8_t* d;
       uint32_t bytes;
       item_addr(k, s, d, bytes);
       mbar_expect_tx(&bars[st], bytes);
-      bulk_load(smem + st * kTmaStage, s, bytes, &bars[st]);
+      bulk_load(smem + st * kStage, s, bytes, &bars[st]);
     }
   }
   bulk_wait_all();
+}
+
+// TMA pipeline shapes: {stages, loads in flight, stage bytes, CTAs per SM}.
+// Bytes in flight per SM = loads in flight x stage bytes x CTAs per SM.
+template <int STAGES, int AHEAD, int STAGE_BYTES>
+int launch_tma(const SlabCopy& c, int dev, int ctas_per_sm, cudaStream_t s) {
+  constexpr int kSmem = STAGES * STAGE_BYTES;
+  static bool attr_set[64] = {false};
+  if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+    KVX_CUDA(cudaFuncSetAttribute(copy_tma_kernel<STAGES, AHEAD, STAGE_BYTES>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr_set[dev] = true;
+  }
+  const int64_t items = c.planes * c.n * ((c.slab + STAGE_BYTES - 1) / STAGE_BYTES);
+  const int blocks = static_cast<int>(
+      std::min<int64_t>(items, static_cast<int64_t>(sm_count(dev)) * ctas_per_sm));
+  copy_tma_kernel<STAGES, AHEAD, STAGE_BYTES><<<blocks, 32, kSmem, s>>>(c);
+  KVX_LAUNCH_CHECK("copy_tma_kernel");
+  return KVX_OK;
 }
 
 int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
@@ -204,16 +222,16 @@ int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
   if (units == 0 || c.slab == 0) return KVX_OK;
   const int sms = sm_count(dev);
   if (g_copy_impl == 1) {
-    static bool attr_set[64] = {false};
-    if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-      KVX_CUDA(cudaFuncSetAttribute(copy_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kTmaSmem));
-      attr_set[dev] = true;
+    static const int cfg = [] {
+      const char* e = std::getenv("KVX_TMA_CFG");  // tuning knob
+      return e ? std::atoi(e) : 0;
+    }();
+    switch (cfg) {
+      case 1: return launch_tma<8, 4, 16384>(c, dev, 1, s);    // 64 KB in flight / SM
+      case 2: return launch_tma<6, 4, 16384>(c, dev, 2, s);    // 128 KB
+      case 3: return launch_tma<6, 4, 32768>(c, dev, 1, s);    // 128 KB
+      default: return launch_tma<12, 8, 16384>(c, dev, 1, s); // 128 KB, one CTA per SM
     }
-    const int64_t items = units * ((c.slab + kTmaStage - 1) / kTmaStage);
-    const int blocks = static_cast<int>(std::min<int64_t>(items, static_cast<int64_t>(sms)));
-    copy_tma_kernel<<<blocks, 32, kTmaSmem, s>>>(c);
-    KVX_LAUNCH_CHECK("copy_tma_kernel");
   } else {
     const int64_t items = units * ((c.slab + kLsuItem - 1) / kLsuItem);
     const int blocks =
