@@ -226,11 +226,16 @@ int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
       const char* e = std::getenv("KVX_TMA_CFG");  // tuning knob
       return e ? std::atoi(e) : 0;
     }();
+    // One issuing thread per CTA is the limiter with a single CTA per SM
+    // (r01 sweep: 12x16K/8 ahead, 1 CTA/SM = 0.55 of HBM; 6x16K/4 ahead,
+    // 2 CTAs/SM = 0.92), so the default runs several CTAs per SM.
     switch (cfg) {
-      case 1: return launch_tma<8, 4, 16384>(c, dev, 1, s);    // 64 KB in flight / SM
-      case 2: return launch_tma<6, 4, 16384>(c, dev, 2, s);    // 128 KB
+      case 1: return launch_tma<8, 4, 16384>(c, dev, 1, s);    //  64 KB in flight / SM
       case 3: return launch_tma<6, 4, 32768>(c, dev, 1, s);    // 128 KB
-      default: return launch_tma<12, 8, 16384>(c, dev, 1, s); // 128 KB, one CTA per SM
+      case 4: return launch_tma<4, 2, 16384>(c, dev, 4, s);    // 128 KB
+      case 5: return launch_tma<6, 4, 16384>(c, dev, 3, s);    // 192 KB
+      case 6: return launch_tma<12, 8, 16384>(c, dev, 1, s);   // 128 KB, one CTA per SM
+      default: return launch_tma<6, 4, 16384>(c, dev, 2, s);   // 128 KB
     }
   } else {
     const int64_t items = units * ((c.slab + kLsuItem - 1) / kLsuItem);
