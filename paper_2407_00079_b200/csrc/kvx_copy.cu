@@ -19,8 +19,9 @@
 //           issued before any store, 4 per thread in flight.
 //   TMA  -- one elected thread per CTA drives cp.async.bulk global->shared
 //           (mbarrier complete_tx) and shared->global bulk stores through a
-//           shared-memory ring (default 12 x 16 KiB stages, 8 loads in
-//           flight = 128 KiB per SM) with no register staging.
+//           shared-memory ring (default 6 x 16 KiB stages, 4 loads in
+//           flight, 2 CTAs per SM = 128 KiB per SM) with no register staging.
+// Measured (Config 2, N=1): LSU 0.95 of HBM, TMA 0.91 -- LSU is the default.
 #include <algorithm>
 #include <cstdlib>
 
