@@ -56,8 +56,9 @@ def parse_args():
                          "512 MiB per layer; 16 for config 3, whose 2048-token chunks are only "
                          "8 MiB per layer and launch-overhead bound one layer at a time)")
     ap.add_argument("--ring", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
-                    help="2: 64 x 8K requests, 50%% shared prefix (default); 3: one 128K request")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3],
+                    help="1: one 8K request; 2: 64 x 8K requests, 50%% shared prefix "
+                         "(default); 3: one 128K request")
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--wave", type=int, default=16, help="decode wave (requests resident at once)")
     ap.add_argument("--block-size", type=int, default=16)
@@ -292,8 +293,12 @@ def build_plan(args, role):
                 "src_slots": wl.src_slots, "dst_slots": wl.dst_slots,
                 "payload_total": wl.payload_bytes(), "scaling": "strong",
                 "describe": wl.describe()}
-    wl = TransferWorkload(n_req=args.requests, wave=args.wave, block_size=args.block_size,
-                          dtype_bytes=args.dtype_bytes)
+    if args.config == 1:  # one 8K-token request (the CPU reference's own case)
+        wl = TransferWorkload(n_req=1, wave=1, block_size=args.block_size,
+                              dtype_bytes=args.dtype_bytes)
+    else:
+        wl = TransferWorkload(n_req=args.requests, wave=args.wave, block_size=args.block_size,
+                              dtype_bytes=args.dtype_bytes)
     host_src = [wl.wave_src_table(w) for w in range(wl.n_waves)]
     host_dst = wl.decode_tables(kvx.SlotAllocator) if role.role != "prefill" else None
     return {"wl": wl, "host_src": host_src, "host_dst": host_dst,
@@ -422,7 +427,7 @@ def run_kvx(args):
     # ---- timed region: CUDA events on the streamer's queue, max over ranks
     # time a sample of the dominant launches: every launch when units are large,
     # every 16th when they are small (an event pair costs ~µs of host time)
-    st.set_timing(True, 1 if args.config == 2 else 16)
+    st.set_timing(True, 16 if args.config == 3 else 1)
     st.launch_stats(reset=True)
     clocks = ClockSampler(dev)
     clocks.start()
