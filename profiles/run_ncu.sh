@@ -1,7 +1,7 @@
 #!/bin/bash
 # ncu evidence for the bench kernels (run on the B200 box via gpurun; 1 GPU).
 # Each ncu command is preceded by the same command run plainly (must exit 0).
-# Outputs land in gpurun_out/; summaries are copied into profiles/ by hand.
+# Outputs land in gpurun_out/; summaries go to profiles/ via summarize_ncu.py.
 set -e
 mkdir -p gpurun_out
 SMALL="--requests 16 --wave 16 --steps 2 --warmup 3 --no-match --no-cpu-baseline --no-e2e"
@@ -20,5 +20,5 @@ ncu --set full --clock-control none --import-source on -k regex:copy_lsu -s 250 
 # 3. full set on the stage-1 kernels (block hash + prefix match, Config 4 batch)
 python bench.py $MATCH > gpurun_out/ncu_plain_match.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"block_hash|match_kernel" \
-    -s 2 -c 2 -o gpurun_out/prof_match_${TAG} python bench.py $MATCH > gpurun_out/ncu_match.log 2>&1
+    -s 3 -c 3 -o gpurun_out/prof_match_${TAG} python bench.py $MATCH > gpurun_out/ncu_match.log 2>&1
 echo done
