@@ -264,8 +264,20 @@ CachePool::AdmitResult CachePool::admit_and_touch(std::span<const BlockId> block
   return admit_and_touch(blocks, 0, 0);
 }
 
+namespace {
+// INT64_MIN / INT64_MIN+1 are the device index's empty / tombstone markers
+// (include/kvx.h); the only keys this block manager cannot hold.
+void reject_sentinels(std::span<const BlockId> blocks) {
+  for (BlockId id : blocks)
+    if (id <= KVX_KEY_TOMBSTONE)
+      throw ValidationError("block id " + std::to_string(id) +
+                            " is reserved by the GPU block index (INT64_MIN, INT64_MIN+1)");
+}
+}  // namespace
+
 CachePool::AdmitResult CachePool::admit_and_touch(std::span<const BlockId> blocks,
                                                   std::size_t skip_begin, std::size_t skip_end) {
+  reject_sentinels(blocks);
   AdmitResult r;
   ++guard_epoch_;
   for (BlockId id : blocks) {  // the whole chain is protected, skip range included
@@ -297,6 +309,7 @@ CachePool::AdmitResult CachePool::admit_and_touch(std::span<const BlockId> block
 
 std::vector<BlockId> CachePool::insert_replicated(std::span<const BlockId> blocks,
                                                   std::size_t chain_offset) {
+  reject_sentinels(blocks);
   std::vector<BlockId> evicted, inserted;
   ++guard_epoch_;
   for (BlockId id : blocks) {
