@@ -598,16 +598,28 @@ def bench_match(args, dev, rank, world, role):
     from paper_2407_00079_b200.cluster import max_over_ranks, sum_over_ranks
     from paper_2407_00079_b200.workloads import MatchWorkload
 
+    import torch.distributed as dist
+
     mw = MatchWorkload().build()
     d = f"cuda:{dev}"
     s = torch.cuda.Stream(dev)
+    n_sess = len(mw.session_ids)
+
+    def instance_keys(inst: int, n_inst: int, warm_keys, warm_ko):
+        """Prefill instance `inst` of n_inst holds the earlier turns of every
+        n_inst-th session, topped up with its own unrelated keys to pool_keys."""
+        ko = warm_ko.cpu().numpy()
+        parts = [warm_keys[int(ko[j]):int(ko[j + 1])] for j in range(n_sess) if j % n_inst == inst]
+        own = torch.cat(parts)[: mw.pool_keys] if parts else warm_keys[:0]
+        filler = torch.as_tensor(mw.filler_keys(mw.pool_keys - own.numel(), salt=inst), device=d)
+        return torch.cat([own, filler])
+
     with torch.cuda.stream(s):
         warm_tok = torch.as_tensor(mw.warm_tokens, device=d)
         warm_off = torch.as_tensor(mw.warm_tok_off, device=d)
-        wkeys, _ = pkg.chain_hash_batch(warm_tok, warm_off, mw.block_size, stream=s)
-        wkeys = wkeys[: mw.pool_keys]
-        filler = torch.as_tensor(mw.filler_keys(mw.pool_keys - wkeys.numel()), device=d)
-        index_keys = torch.cat([wkeys, filler])
+        wkeys, wko = pkg.chain_hash_batch(warm_tok, warm_off, mw.block_size, stream=s)
+        # one prefill instance per GPU (SURVEY 8(e) case ii): this rank's index
+        index_keys = instance_keys(rank, world, wkeys, wko)
         idx = pkg.BlockIndex(dev, mw.pool_keys)
         idx.insert(index_keys, stream=s)
         tokens = torch.as_tensor(mw.tokens, device=d)
@@ -617,6 +629,7 @@ def bench_match(args, dev, rank, world, role):
         keys = torch.empty(n_blocks, dtype=torch.int64, device=d)
         best_len = torch.empty(mw.n_req, dtype=torch.int64, device=d)
         best_id = torch.empty(mw.n_req, dtype=torch.int32, device=d)
+        packed = torch.empty(mw.n_req, dtype=torch.int64, device=d)
     s.synchronize()
     st = idx.stats()
     assert st["live"] == mw.pool_keys, st
@@ -626,17 +639,39 @@ def bench_match(args, dev, rank, world, role):
     tok_bytes = mw.tokens.nbytes
 
     def step(timed):
+        nonlocal best_len, best_id
         a = th.start(s) if timed else None
         pkg.chain_hash_batch(tokens, tok_off, mw.block_size, key_off=key_off, keys=keys, stream=s)
         th.stop(s, a, tok_bytes + 8 * n_blocks)
         b = tm.start(s) if timed else None
-        pkg.match_prefix_batch([idx], [0], keys, key_off, want_lens=False, stream=s,
-                               out=(None, best_len, best_id))
+        if world == 1:
+            pkg.match_prefix_batch([idx], [0], keys, key_off, want_lens=False, stream=s,
+                                   out=(None, best_len, best_id))
+        else:  # local best per request, then the cross-GPU exchange: all-reduce(MAX)
+            pkg.kvx.match_prefix_packed([idx], [rank], keys, key_off, out=packed, stream=s)
         tm.stop(s, b, 0)
+        if world > 1:
+            with torch.cuda.stream(s):
+                dist.all_reduce(packed, op=dist.ReduceOp.MAX)
+            best_len, best_id = pkg.kvx.best_unpack(packed, stream=s)
 
     for _ in range(args.warmup):
         step(False)
     s.synchronize()
+    if world > 1 and rank == 0:
+        # parity of the exchange: all N instances on one GPU, one batched query
+        with torch.cuda.stream(s):
+            all_idx = []
+            for i in range(world):
+                ix = pkg.BlockIndex(dev, mw.pool_keys)
+                ix.insert(instance_keys(i, world, wkeys, wko), stream=s)
+                all_idx.append(ix)
+            _, ref_len, ref_id = pkg.match_prefix_batch(all_idx, list(range(world)), keys,
+                                                        key_off, want_lens=False, stream=s)
+        s.synchronize()
+        assert torch.equal(ref_len, best_len) and torch.equal(ref_id, best_id), \
+            "cross-GPU best-match parity"
+        del all_idx
     # parity spot check against the oracle restatement on the first requests
     from oracle import Oracle
     o = Oracle()
@@ -652,7 +687,9 @@ def bench_match(args, dev, rank, world, role):
     e1.record(s)
     s.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
-    total_blocks = sum_over_ranks(float(n_blocks), d)
+    # every rank answers the same batch for its own instance; the all-reduce
+    # makes it one global find_best_prefix_match over `world` instances
+    total_blocks = float(n_blocks)
     value = total_blocks / (ms / 1e3)
     hs, ms_match = th.summary(), tm.summary()
     match_bytes = 24 * n_probes
@@ -684,7 +721,10 @@ def bench_match(args, dev, rank, world, role):
     return {
         "metric": "prefix-match blocks/s (batched block hash + prefix match)",
         "value": value, "unit": "blocks/s", "ms_per_step": ms,
-        "config": {**mw.describe(), "instances": 1, "replicas": world},
+        "config": {**mw.describe(), "instances": world,
+                   "layout": ("one instance index" if world == 1 else
+                              "one prefill instance index per GPU; per-request best combined "
+                              "by all-reduce(MAX) over packed (len<<32 | ~id) words (NCCL)")},
         "kernels": {
             "block_hash_kernel": {"avg_ms": hs["avg_ms"], "bytes": hs["avg_algorithmic_bytes"],
                                   "achieved_gbs": hash_gbs,

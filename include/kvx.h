@@ -122,6 +122,16 @@ int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids,
                            int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
                            void* stream);
 
+/* Same query, leaving per request the packed word (len << 32 | ~ordered(id))
+ * whose MAXIMUM is the best match with the lowest-id tie-break: instances
+ * held by different GPUs combine with one all-reduce(MAX) over these words
+ * (SURVEY 8(e) case ii), then kvx_best_unpack. */
+int kvx_match_prefix_packed(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+                            const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+                            uint64_t* d_packed, void* stream);
+int kvx_best_unpack(const uint64_t* d_packed, int64_t n_req, int64_t* d_best_len,
+                    int32_t* d_best_id, void* stream);
+
 /* ---- paged KV pool ------------------------------------------------------ */
 
 /* HBM layout: base[((layer*2 + kv)*slots + slot) * slab], slab =

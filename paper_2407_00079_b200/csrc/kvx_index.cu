@@ -180,6 +180,7 @@ struct MatchParams {
   uint64_t mask[KVX_MAX_INSTANCES];
   int32_t ids[KVX_MAX_INSTANCES];
   int32_t n_inst;
+  int32_t packed_only;  // leave the packed (len<<32 | ~id) word for a cross-GPU MAX
 };
 
 // U independent probe chains per lane: every chain's next slot load is issued
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
     if (lane == 0) {
       if (len_out) len_out[t] = len;
       if (best_len) {
-        if (p.n_inst == 1) {
+        if (p.n_inst == 1 && !p.packed_only) {
           best_len[r] = len;
           best_id[r] = p.ids[0];
         } else {
@@ -283,11 +284,12 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
   }
 }
 
-__global__ void unpack_best_kernel(int64_t* __restrict__ best_len, int32_t* __restrict__ best_id,
-                                   int64_t n_req) {
+// packed may alias best_len (in-place unpack).
+__global__ void unpack_best_kernel(const unsigned long long* packed, int64_t* best_len,
+                                   int32_t* __restrict__ best_id, int64_t n_req) {
   for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < n_req;
        r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long v = static_cast<unsigned long long>(best_len[r]);
+    const unsigned long long v = packed[r];
     best_len[r] = static_cast<int64_t>(v >> 32);
     best_id[r] = static_cast<int32_t>(~static_cast<uint32_t>(v & 0xffffffffu) ^ 0x80000000u);
   }
@@ -375,6 +377,11 @@ int ensure_room(kvx_index* x, int64_t n, cudaStream_t s) {
   x->used_ub = live;
   return KVX_OK;
 }
+
+int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+               const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+               int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id, bool packed_only,
+               void* stream);
 
 }  // namespace
 
@@ -519,8 +526,46 @@ int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids,
               "kvx_match_prefix_batch: best_len and best_id go together");
   if (n_req == 0) return KVX_OK;
   KVX_REQUIRE(d_keys && d_key_off, "kvx_match_prefix_batch: NULL keys");
+  return match_impl(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out, d_best_len,
+                    d_best_id, false, stream);
+}
+
+int kvx_match_prefix_packed(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+                            const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+                            uint64_t* d_packed, void* stream) {
+  KVX_REQUIRE(n_inst >= 1, "find_best_prefix_match: empty prefill pool");
+  KVX_REQUIRE(n_inst <= KVX_MAX_INSTANCES, "kvx_match_prefix_packed: too many instances");
+  KVX_REQUIRE(idx != nullptr && inst_ids != nullptr, "kvx_match_prefix_packed: NULL instances");
+  KVX_REQUIRE(n_req >= 0, "kvx_match_prefix_packed: n_req must be >= 0");
+  if (n_req == 0) return KVX_OK;
+  KVX_REQUIRE(d_keys && d_key_off && d_packed, "kvx_match_prefix_packed: NULL array");
+  return match_impl(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, nullptr,
+                    reinterpret_cast<int64_t*>(d_packed), nullptr, true, stream);
+}
+
+int kvx_best_unpack(const uint64_t* d_packed, int64_t n_req, int64_t* d_best_len,
+                    int32_t* d_best_id, void* stream) {
+  KVX_REQUIRE(n_req >= 0, "kvx_best_unpack: n_req must be >= 0");
+  if (n_req == 0) return KVX_OK;
+  KVX_REQUIRE(d_packed && d_best_len && d_best_id, "kvx_best_unpack: NULL array");
+  int dev = 0;
+  KVX_CUDA(cudaGetDevice(&dev));
+  unpack_best_kernel<<<grid_for(n_req, 256, dev), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const unsigned long long*>(d_packed), d_best_len, d_best_id, n_req);
+  KVX_LAUNCH_CHECK("unpack_best_kernel");
+  return KVX_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+               const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+               int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id, bool packed_only,
+               void* stream) {
   MatchParams p{};
   p.n_inst = static_cast<int32_t>(n_inst);
+  p.packed_only = packed_only ? 1 : 0;
   const int dev = idx[0] ? idx[0]->device : -1;
   for (int64_t i = 0; i < n_inst; ++i) {
     KVX_REQUIRE(idx[i] != nullptr, "kvx_match_prefix_batch: NULL index");
@@ -531,7 +576,7 @@ int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids,
   }
   DeviceGuard g(dev);
   cudaStream_t s = as_stream(stream);
-  if (d_best_len && n_inst > 1)
+  if (d_best_len && (n_inst > 1 || packed_only))
     KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
   const int threads = 256;
   const int64_t tasks = n_req * n_inst;
@@ -541,11 +586,11 @@ int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids,
   match_kernel<<<blocks, threads, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out, d_best_len,
                                           d_best_id);
   KVX_LAUNCH_CHECK("match_kernel");
-  if (d_best_len && n_inst > 1) {
-    unpack_best_kernel<<<grid_for(n_req, 256, dev), 256, 0, s>>>(d_best_len, d_best_id, n_req);
+  if (d_best_len && n_inst > 1 && !packed_only) {
+    unpack_best_kernel<<<grid_for(n_req, 256, dev), 256, 0, s>>>(
+        reinterpret_cast<const unsigned long long*>(d_best_len), d_best_len, d_best_id, n_req);
     KVX_LAUNCH_CHECK("unpack_best_kernel");
   }
   return KVX_OK;
 }
-
-}  // extern "C"
+}  // namespace

@@ -83,6 +83,9 @@ _sig("kvx_index_stats", C.c_int, _vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTE
      C.POINTER(_i64), _vp)
 _sig("kvx_match_prefix_batch", C.c_int, C.POINTER(_vp), C.POINTER(_i32), _i64, _vp, _vp, _i64,
      _vp, _vp, _vp, _vp)
+_sig("kvx_match_prefix_packed", C.c_int, C.POINTER(_vp), C.POINTER(_i32), _i64, _vp, _vp, _i64,
+     _vp, _vp)
+_sig("kvx_best_unpack", C.c_int, _vp, _i64, _vp, _vp, _vp)
 _sig("kvx_pool_create", C.c_int, C.POINTER(KvxPoolDesc), C.POINTER(_vp))
 _sig("kvx_pool_create_view", C.c_int, C.POINTER(KvxPoolDesc), _vp, C.POINTER(_vp))
 _sig("kvx_pool_destroy", C.c_int, _vp)
@@ -273,6 +276,31 @@ def match_prefix_batch(indices: Sequence[BlockIndex], inst_ids: Sequence[int], k
                                     _ptr(key_off), n_req, _ptr(lens) if lens is not None else None,
                                     _ptr(best_len), _ptr(best_id), _stream(stream)))
     return lens, best_len, best_id
+
+
+def match_prefix_packed(indices: Sequence[BlockIndex], inst_ids: Sequence[int],
+                        keys: torch.Tensor, key_off: torch.Tensor, out: Optional[torch.Tensor] = None,
+                        stream=None) -> torch.Tensor:
+    """Per request the packed best word (len << 32 | ~ordered(id)), an int64
+    tensor whose element-wise MAX over GPUs (all-reduce) is the global
+    find_best_prefix_match; decode with best_unpack."""
+    n_inst = len(indices)
+    n_req = len(key_off) - 1
+    arr = (_vp * max(n_inst, 1))(*[i.h for i in indices])
+    ids = (_i32 * max(n_inst, 1))(*[int(i) for i in inst_ids])
+    if out is None:
+        out = torch.empty(n_req, dtype=torch.int64, device=keys.device)
+    check(_L.kvx_match_prefix_packed(arr, ids, n_inst, _ptr(keys) if keys.numel() else None,
+                                     _ptr(key_off), n_req, _ptr(out), _stream(stream)))
+    return out
+
+
+def best_unpack(packed: torch.Tensor, stream=None):
+    n = packed.numel()
+    best_len = torch.empty(n, dtype=torch.int64, device=packed.device)
+    best_id = torch.empty(n, dtype=torch.int32, device=packed.device)
+    check(_L.kvx_best_unpack(_ptr(packed), n, _ptr(best_len), _ptr(best_id), _stream(stream)))
+    return best_len, best_id
 
 
 # ---- paged KV pool and stages 2/4 ---------------------------------------------

@@ -211,10 +211,11 @@ class MatchWorkload:
         lens = np.diff(self.tok_off)
         return int(((lens + self.block_size - 1) // self.block_size).sum())
 
-    def filler_keys(self, n: int) -> np.ndarray:
+    def filler_keys(self, n: int, salt: int = 0) -> np.ndarray:
         """Unrelated resident keys (never equal to a chain key with overwhelming
-        probability: they are drawn uniformly from [2^62, 2^63 - 2^20))."""
-        rng = np.random.default_rng(self.filler_rng_seed)
+        probability: they are drawn uniformly from [2^62, 2^63 - 2^20));
+        `salt` gives each prefill instance its own."""
+        rng = np.random.default_rng(self.filler_rng_seed + salt)
         return rng.integers(1 << 62, (1 << 63) - (1 << 20), size=n, dtype=np.int64)
 
     def describe(self) -> dict:

@@ -139,6 +139,28 @@ def test_match_batch_random_vs_oracle(kvx, oracle_lib, n_inst):
     assert np.array_equal(bi.cpu().numpy(), wbi)
 
 
+def test_packed_best_combines_like_one_batch(kvx, oracle_lib):
+    """Instances spread over 'GPUs': element-wise MAX of per-instance packed
+    words (what all-reduce(MAX) does) == the multi-instance batched result."""
+    rng = np.random.default_rng(31)
+    reqs = _forest(rng, 200, 6, 0, 300)
+    key_off = np.concatenate([[0], np.cumsum([len(r) for r in reqs])]).astype(np.int64)
+    keys = np.concatenate(reqs).astype(np.int64)
+    contents = [np.concatenate([reqs[j][: int(rng.integers(0, len(reqs[j]) + 1))]
+                                for j in rng.choice(len(reqs), 15, replace=False)])
+                for _ in range(5)]
+    ids = [4, 0, 3, 1, 2]
+    idx = [_index(kvx, c) for c in contents]
+    k, ko = _t(keys, torch.int64), _t(key_off, torch.int64)
+    _, bl, bi = kvx.match_prefix_batch(idx, ids, k, ko, want_lens=False)
+    packed = torch.stack([kvx.kvx.match_prefix_packed([ix], [i], k, ko) for ix, i in zip(idx, ids)])
+    gl, gi = kvx.kvx.best_unpack(packed.max(dim=0).values)
+    assert torch.equal(gl, bl) and torch.equal(gi, bi)
+    sets = [oracle_lib.make_set(c) for c in contents]
+    _, wbl, wbi = oracle_lib.match_prefix_batch(sets, ids, keys, key_off)
+    assert np.array_equal(gl.cpu().numpy(), wbl) and np.array_equal(gi.cpu().numpy(), wbi)
+
+
 def test_index_erase_lookup_growth(kvx, oracle_lib):
     rng = np.random.default_rng(5)
     idx = kvx.BlockIndex(0, 16)  # must grow several times
