@@ -679,6 +679,9 @@ def bench_match(args, dev, rank, world, role):
     assert np.array_equal(keys[: ko_ref[-1]].cpu().numpy(), k_ref), "hash parity"
     lens_all = best_len.cpu().numpy()
     n_probes = int(np.minimum(lens_all + 1, np.diff(key_off.cpu().numpy())).sum())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()  # all ranks enter the timed region together (the all-reduce pairs them)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(s)
@@ -698,6 +701,9 @@ def bench_match(args, dev, rank, world, role):
     pin_tok = torch.as_tensor(mw.tokens).pin_memory()
     out_len = torch.empty(mw.n_req, dtype=torch.int64).pin_memory()
     out_id = torch.empty(mw.n_req, dtype=torch.int32).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(s)
