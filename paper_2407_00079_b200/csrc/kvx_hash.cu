@@ -44,6 +44,9 @@ namespace {
 
 constexpr int kHashThreads = 256;  // 8 warps: warp 0 folds (when assigned), 1..7 produce
 constexpr int kFoldBatch = 16;
+#ifndef KVX_HASH_MIN_CTAS
+#define KVX_HASH_MIN_CTAS 3  // resident CTAs per SM (r01 sweep: 3 best; more spills or slows the fold)
+#endif
 
 __device__ __forceinline__ int64_t fold_tokens_scalar(const int32_t* __restrict__ t, int n) {
   int64_t h = 0;
@@ -194,7 +197,7 @@ __device__ __forceinline__ void fold_requests(const int64_t* __restrict__ key_of
 // joins the folding of whatever is still unclaimed.
 constexpr int kFoldWarps = 4;
 
-__global__ void __launch_bounds__(kHashThreads) block_hash_fused_kernel(
+__global__ void __launch_bounds__(kHashThreads, KVX_HASH_MIN_CTAS) block_hash_fused_kernel(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
     int bs, const int64_t* __restrict__ key_off, int64_t* keys, unsigned long long* ws,
     int fold_sms) {
