@@ -132,6 +132,58 @@ int kvx_match_prefix_packed(const kvx_index* const* idx, const int32_t* inst_ids
 int kvx_best_unpack(const uint64_t* d_packed, int64_t n_req, int64_t* d_best_len,
                     int32_t* d_best_id, void* stream);
 
+/* ---- batched Conductor scoring (kvcache-centric schedule, FP64) -------- */
+
+/* Mirrors of kvcsim::PerfModelParams (proj/include/kvcsim/perf_model.hpp:13-26),
+ * the SLO / conductor knobs schedule() reads, and the two snapshot structs
+ * (proj/include/kvcsim/conductor.hpp:41-55). */
+typedef struct {
+  double alpha_mlp, beta_attn, gamma_decode, delta_decode, epsilon_decode;
+  double kv_bytes_per_token, link_bandwidth, load_bandwidth;
+  int64_t prefill_chunk, cpp_group_size;
+} kvx_perf_params;
+
+typedef struct {
+  double l_ttft_ms, l_tbt_ms, kvcache_balancing_threshold, now_ms;
+  int64_t block_size;
+} kvx_sched_params;
+
+typedef struct {
+  int32_t id;
+  int32_t pad_;
+  double busy_until_ms, sender_busy_until_ms, queued_work_ms;
+} kvx_prefill_snapshot;
+
+typedef struct {
+  int32_t id;
+  int32_t pad_;
+  int64_t batch_size, resident_kv_tokens;
+} kvx_decode_snapshot;
+
+typedef struct {
+  int32_t accepted;
+  int32_t reject_reason; /* 0 none, 1 TTFT SLO, 2 TBT SLO (conductor.cpp:245-255) */
+  int32_t prefill_id, decode_id;
+  int64_t local_prefix_blocks, used_prefix_blocks;
+  int64_t best_prefix_blocks;
+  int32_t best_instance_id;
+  int32_t migrate;         /* hot-spot migration planned (conductor.cpp:257-260) */
+  int32_t migrate_source;
+  int32_t pad_;
+  int64_t migrate_prefix_blocks;
+  double queue_ms, transfer_ms, exec_ms, ttft_ms, tbt_ms;
+} kvx_sched_decision;
+
+/* schedule() for kKvcacheCentric (proj/src/conductor.cpp:126-262) applied to
+ * n_req requests against ONE snapshot: d_match_len is the n_req x n_prefill
+ * matrix from kvx_match_prefix_batch (same instance order as d_prefill).  All
+ * doubles are bit-identical to the reference's host arithmetic. */
+int kvx_schedule_batch(const kvx_perf_params* perf, const kvx_sched_params* sp,
+                       const kvx_prefill_snapshot* d_prefill, int64_t n_prefill,
+                       const kvx_decode_snapshot* d_decode, int64_t n_decode,
+                       const int64_t* d_input_len, const int64_t* d_match_len, int64_t n_req,
+                       kvx_sched_decision* d_out, void* stream);
+
 /* ---- paged KV pool ------------------------------------------------------ */
 
 /* HBM layout: base[((layer*2 + kv)*slots + slot) * slab], slab =

@@ -217,6 +217,34 @@ class RefLib:
     def chain_hash(self, prev: int, content: int) -> int:
         return int(self.L.kvref_chain_hash(int(prev), int(content) & 0xFFFFFFFFFFFFFFFF))
 
+    def schedule(self, perf8, chunk, stages, l_ttft, l_tbt, threshold, block_size, now, pools,
+                 ids, busy, sender, queued, dids, dbatch, dkv, input_len, keys):
+        """kvref::schedule(kKvcacheCentric) for one request -> (ints[9], doubles[5])."""
+        f = self.L.kvref_schedule
+        if not getattr(f, "_typed", False):
+            d, i64, i32 = C.POINTER(C.c_double), _i64p, _i32p
+            f.restype = C.c_int
+            f.argtypes = [d, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int64,
+                          C.c_double, C.POINTER(C.c_void_p), i32, d, d, d, C.c_int64, i32, i64,
+                          i64, C.c_int64, C.c_int64, i64, C.c_int64, i64, d]
+            f._typed = True
+        a = lambda x, t: np.ascontiguousarray(x, dtype=t)  # noqa: E731
+        pf, b, s, q = (a(perf8, np.float64), a(busy, np.float64), a(sender, np.float64),
+                       a(queued, np.float64))
+        ii, di, db, dk, k = (a(ids, np.int32), a(dids, np.int32), a(dbatch, np.int64),
+                             a(dkv, np.int64), a(keys, np.int64))
+        arr = (C.c_void_p * len(pools))(*[p.h for p in pools])
+        oi = np.zeros(9, dtype=np.int64)
+        od = np.zeros(5, dtype=np.float64)
+        dp = C.POINTER(C.c_double)
+        rc = f(pf.ctypes.data_as(dp), chunk, stages, l_ttft, l_tbt, threshold, block_size, now, arr,
+               _p(ii, _i32p), b.ctypes.data_as(dp), s.ctypes.data_as(dp), q.ctypes.data_as(dp),
+               len(pools), _p(di, _i32p), _p(db, _i64p), _p(dk, _i64p), len(di), input_len,
+               _p(k, _i64p), len(k), _p(oi, _i64p), od.ctypes.data_as(dp))
+        if rc != 0:
+            raise ValueError("ValidationError")
+        return oi, od
+
     def pool(self, capacity=None, policy="lru"):
         return RefPool(self, capacity, policy)
 

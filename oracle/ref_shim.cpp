@@ -182,6 +182,71 @@ void kvref_block_hash_mt(const int32_t* tokens, const int64_t* tok_off, int64_t 
   for (auto& x : th) x.join();
 }
 
+/* kvref::schedule(..., kKvcacheCentric) for one request (conductor.cpp:126-262).
+ * perf8 = alpha, beta, gamma, delta, epsilon, kv_bytes_per_token, link_bw, load_bw.
+ * out_i = accepted, reject_reason(0/1/2), prefill_id, decode_id, local_prefix,
+ *         used_prefix, migrate, migrate_source, migrate_prefix_blocks
+ * out_d = queue_ms, transfer_ms, exec_ms, ttft_ms, tbt_ms.  Returns -1 on
+ * ValidationError. */
+int kvref_schedule(const double* perf8, int64_t chunk, int64_t stages, double l_ttft,
+                   double l_tbt, double threshold, int64_t block_size, double now,
+                   void* const* pools, const int32_t* ids, const double* busy,
+                   const double* sender, const double* queued, int64_t n_pre,
+                   const int32_t* dids, const int64_t* dbatch, const int64_t* dkv, int64_t n_dec,
+                   int64_t input, const int64_t* keys, int64_t n_keys, int64_t* out_i,
+                   double* out_d) {
+  kvref::PerfModelParams p;
+  p.alpha_mlp = perf8[0];
+  p.beta_attn = perf8[1];
+  p.gamma_decode = perf8[2];
+  p.delta_decode = perf8[3];
+  p.epsilon_decode = perf8[4];
+  p.kv_bytes_per_token = perf8[5];
+  p.link_bandwidth = perf8[6];
+  p.load_bandwidth = perf8[7];
+  p.prefill_chunk = chunk;
+  p.cpp_group_size = stages;
+  std::vector<kvref::PrefillSnapshot> pre;
+  for (int64_t i = 0; i < n_pre; ++i)
+    pre.push_back({ids[i], static_cast<const kvref::CachePool*>(pools[i]), busy[i], sender[i],
+                   queued[i]});
+  std::vector<kvref::DecodeSnapshot> dec;
+  for (int64_t i = 0; i < n_dec; ++i) dec.push_back({dids[i], dbatch[i], dkv[i], std::nullopt});
+  kvref::SLOConfig slo;
+  slo.l_ttft_ms = l_ttft;
+  slo.l_tbt_ms = l_tbt;
+  kvref::ConductorConfig cc;
+  cc.kvcache_balancing_threshold = threshold;
+  cc.block_size = block_size;
+  kvref::RequestRecord rec;
+  rec.input_length = input;
+  rec.output_length = 1;
+  rec.hash_ids.assign(keys, keys + n_keys);
+  const kvref::ScheduleContext ctx{pre, dec, slo, cc, p, now};
+  try {
+    const auto d = kvref::schedule(rec, ctx, kvref::SchedulerChoice::kKvcacheCentric);
+    out_i[0] = d.accepted;
+    out_i[1] = d.reject_reason == kvref::RejectReason::kTtftSlo   ? 1
+               : d.reject_reason == kvref::RejectReason::kTbtSlo ? 2
+                                                                  : 0;
+    out_i[2] = d.prefill_id;
+    out_i[3] = d.decode_id;
+    out_i[4] = static_cast<int64_t>(d.local_prefix_blocks);
+    out_i[5] = static_cast<int64_t>(d.used_prefix_blocks);
+    out_i[6] = d.migration.has_value();
+    out_i[7] = d.migration ? d.migration->source_id : 0;
+    out_i[8] = d.migration ? static_cast<int64_t>(d.migration->prefix_blocks) : 0;
+    out_d[0] = d.queue_ms;
+    out_d[1] = d.transfer_ms;
+    out_d[2] = d.exec_ms;
+    out_d[3] = d.estimated_ttft_ms;
+    out_d[4] = d.estimated_tbt_ms;
+    return 0;
+  } catch (const kvref::ValidationError&) {
+    return -1;
+  }
+}
+
 /* Bulk-load a reference pool (setup for the CPU baseline; not timed). */
 void kvref_pool_insert_many(void* pool, const int64_t* keys, int64_t n) {
   auto* p = static_cast<kvref::CachePool*>(pool);

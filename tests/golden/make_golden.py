@@ -233,6 +233,77 @@ def cachepool_fixture(ref: RefLib) -> None:
     )
 
 
+def schedule_fixture(ref: RefLib) -> None:
+    """Randomized cluster snapshots shaped like acceptance criterion 4's
+    make_random_state (proj/tests/acceptance_main.cpp:237-302), 4 requests per
+    snapshot; expected decisions from kvref::schedule(kKvcacheCentric)."""
+    rng = np.random.default_rng(4004)
+    S, R = 300, 4
+    rows = {k: [] for k in ("perf", "ints", "dbl", "inst_keys", "inst_off", "inst_ids", "busy",
+                            "sender", "queued", "n_inst", "dec_ids", "dec_batch", "dec_kv",
+                            "n_dec", "req_input", "req_keys", "req_off", "exp_i", "exp_d")}
+    rows["inst_off"].append(0)
+    rows["req_off"].append(0)
+    for s in range(S):
+        perf = [0.01 + rng.random() * 0.2, rng.random() * 1e-5, rng.random() * 20.0,
+                rng.random() * 2.0, rng.random(), 1000.0 + rng.random() * 2e5,
+                1e5 + rng.random() * 1e7, 1e5 + rng.random() * 1e7]
+        chunk, stages = int(rng.integers(256, 4097)), int(rng.integers(1, 5))
+        threshold = 1.0 + rng.random() * 7.0
+        l_ttft = 200.0 + rng.random() * 2000.0 if rng.random() < 0.3 else 1e9
+        l_tbt = 5.0 + rng.random() * 50.0 if rng.random() < 0.3 else 1e9
+        now = rng.random() * 200.0
+        blocks = int(rng.integers(1, 25))
+        chain = np.arange(blocks, dtype=np.int64) + s * 1000
+        n_inst = int(rng.integers(2, 17))
+        ids = rng.permutation(n_inst).astype(np.int32)
+        pools = []
+        for i in range(n_inst):
+            warm = int(rng.integers(0, blocks + 1))
+            content = list(chain[:warm]) + [int(x) for x in
+                                            900000 + rng.integers(0, 100, int(rng.integers(0, 7)))]
+            p = ref.pool(None, "lru")
+            if content:
+                p.insert_replicated(np.array(content, dtype=np.int64))
+            pools.append(p)
+            rows["inst_keys"].extend(int(x) for x in content)
+            rows["inst_off"].append(len(rows["inst_keys"]))
+        busy = [rng.random() * 500.0 if rng.random() < 0.5 else 0.0 for _ in range(n_inst)]
+        sender = [rng.random() * 300.0 if rng.random() < 0.5 else 0.0 for _ in range(n_inst)]
+        queued = [rng.random() * 1500.0 for _ in range(n_inst)]
+        n_dec = int(rng.integers(1, 7))
+        dids = rng.permutation(n_dec).astype(np.int32)
+        dbatch = rng.integers(0, 33, n_dec)
+        dkv = rng.integers(0, 200001, n_dec)
+        for _ in range(R):
+            nb = int(rng.integers(1, blocks + 1))
+            keys = np.concatenate([chain[:nb], 5_000_000 + s * 10 + rng.integers(0, 5, 1)])
+            keys = keys[: nb + int(rng.integers(0, 2))]
+            inp = len(keys) * 512 - int(rng.integers(0, 512))
+            ei, ed = ref.schedule(perf, chunk, stages, l_ttft, l_tbt, threshold, 512, now, pools,
+                                  ids, busy, sender, queued, dids, dbatch, dkv, inp, keys)
+            rows["req_input"].append(inp)
+            rows["req_keys"].extend(int(x) for x in keys)
+            rows["req_off"].append(len(rows["req_keys"]))
+            rows["exp_i"].append(ei)
+            rows["exp_d"].append(ed)
+        rows["perf"].append(perf)
+        rows["ints"].append([chunk, stages])
+        rows["dbl"].append([l_ttft, l_tbt, threshold, now])
+        rows["inst_ids"].extend(ids.tolist())
+        rows["busy"].extend(busy)
+        rows["sender"].extend(sender)
+        rows["queued"].extend(queued)
+        rows["n_inst"].append(n_inst)
+        rows["dec_ids"].extend(dids.tolist())
+        rows["dec_batch"].extend(dbatch.tolist())
+        rows["dec_kv"].extend(dkv.tolist())
+        rows["n_dec"].append(n_dec)
+    out = {k: np.array(v) for k, v in rows.items()}
+    out["requests_per_state"] = np.array(R)
+    np.savez_compressed(os.path.join(OUT, "schedule_states.npz"), **out)
+
+
 match_probe_keys: list = []
 match_probe_off: list = [0]
 final_stats: list = []
@@ -246,6 +317,7 @@ def main() -> None:
     block_hash_fixture(ref)
     match_fixture(ref)
     cachepool_fixture(ref)
+    schedule_fixture(ref)
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)), "bytes")
