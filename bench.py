@@ -718,6 +718,65 @@ def bench_match(args, dev, rank, world, role):
     s.synchronize()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1), d) / args.steps
 
+    # batched Conductor scoring: P=8 prefill instances on
+    # this GPU, per-instance match matrix + kvcache-centric schedule of the batch
+    conductor = None
+    if world == 1:
+        from paper_2407_00079_b200 import conductor as cd
+        P = 8
+        with torch.cuda.stream(s):
+            inst = []
+            for i in range(P):
+                ix = pkg.BlockIndex(dev, mw.pool_keys)
+                ix.insert(instance_keys(i, P, wkeys, wko), stream=s)
+                inst.append(ix)
+            lens = torch.empty((mw.n_req, P), dtype=torch.int64, device=d)
+            bl8 = torch.empty(mw.n_req, dtype=torch.int64, device=d)
+            bi8 = torch.empty(mw.n_req, dtype=torch.int32, device=d)
+            inp = tok_off[1:] - tok_off[:-1]
+        rng = np.random.default_rng(8)
+        pre = np.zeros(P, dtype=cd.PREFILL_DT)
+        pre["id"] = np.arange(P)
+        pre["busy_until_ms"] = rng.random(P) * 500
+        pre["sender_busy_until_ms"] = rng.random(P) * 300
+        pre["queued_work_ms"] = rng.random(P) * 1500
+        dec = np.zeros(8, dtype=cd.DECODE_DT)
+        dec["id"] = np.arange(8)
+        dec["batch_size"] = rng.integers(0, 33, 8)
+        dec["resident_kv_tokens"] = rng.integers(0, 200000, 8)
+        perf = cd.PerfParams(cpp_group_size=2)
+        kwargs = dict(perf=perf, l_ttft_ms=30000.0, l_tbt_ms=100.0, threshold=4.0,
+                      block_size=mw.block_size, now_ms=0.0, prefill=pre, decode=dec,
+                      input_len=inp, match_len=lens, stream=s)
+
+        def conduct():
+            pkg.match_prefix_batch(inst, list(range(P)), keys, key_off, stream=s,
+                                   out=(lens, bl8, bi8))
+            return cd.schedule_batch(**kwargs)
+
+        conduct()
+        s.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(s)
+        for _ in range(args.steps):
+            pkg.match_prefix_batch(inst, list(range(P)), keys, key_off, stream=s,
+                                   out=(lens, bl8, bi8))
+        c1.record(s)
+        s.synchronize()
+        match8_ms = c0.elapsed_time(c1) / args.steps
+        t0 = time.perf_counter()
+        dec_out = conduct()
+        call_ms = (time.perf_counter() - t0) * 1e3
+        conductor = {
+            "metric": "kvcache-centric schedule of the batch (match matrix + FP64 scoring)",
+            "instances": P, "requests": mw.n_req, "match_matrix_ms": match8_ms,
+            "match_matrix_blocks_per_s": n_blocks * P / (match8_ms / 1e3),
+            "end_to_end_call_ms": call_ms,
+            "decisions": {"accepted": int(dec_out["accepted"].sum()),
+                          "migrations": int(dec_out["migrate"].sum())},
+            "note": "scoring bit-identical to kvref::schedule (tests/test_gpu_conductor.py)"}
+        del inst
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_match_sample(mw, min(args.cpu_seconds, 10.0))
@@ -743,6 +802,7 @@ def bench_match(args, dev, rank, world, role):
         "e2e": {"value": total_blocks / (e2e_ms / 1e3), "unit": "blocks/s",
                 "h2d_bytes_per_step": int(tok_bytes), "d2h_bytes_per_step": mw.n_req * 12},
         "cpu_baseline": cpu,
+        "conductor_p8": conductor,
     }
 
 
