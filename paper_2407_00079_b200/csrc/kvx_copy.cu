@@ -239,9 +239,14 @@ int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
       default: return launch_tma<6, 4, 16384>(c, dev, 2, s);   // 128 KB
     }
   } else {
+    static const int ctas_per_sm = [] {
+      const char* e = std::getenv("KVX_LSU_CTAS");  // tuning knob (default 4 = 2048 threads/SM)
+      const int v = e ? std::atoi(e) : 4;
+      return v >= 1 && v <= 4 ? v : 4;
+    }();
     const int64_t items = units * ((c.slab + kLsuItem - 1) / kLsuItem);
     const int blocks =
-        static_cast<int>(std::min<int64_t>(items, static_cast<int64_t>(sms) * 4));
+        static_cast<int>(std::min<int64_t>(items, static_cast<int64_t>(sms) * ctas_per_sm));
     copy_lsu_kernel<<<blocks, kLsuThreads, 0, s>>>(c);
     KVX_LAUNCH_CHECK("copy_lsu_kernel");
   }
