@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--impl", default="kvx", choices=["kvx", "reference"])
     ap.add_argument("--mode", default="auto",
                     choices=["auto", "local_fused", "local_staged", "peer_fused", "peer_ce",
-                             "peer_nccl"])
+                             "peer_pull", "peer_nccl"])
     ap.add_argument("--copy-impl", default="lsu", choices=["lsu", "tma"])
     ap.add_argument("--layers-per-chunk", type=int, default=0,
                     help="layers per streamed unit; 0 = auto (1 for config 2, whose units are "
@@ -378,7 +378,7 @@ def run_kvx(args):
             host_dst = peer["tables"]
             st.connect(peer["blob"], {**pool_kw, "slots": plan["dst_slots"]})
         else:
-            st.connect(peer["blob"])
+            st.connect(peer["blob"], {**pool_kw, "slots": plan["src_slots"]})
     main = torch.cuda.Stream(dev)  # torch-owned queue: H2D/D2H, timing events; the streamer
     # queues are ordered against it with st.after(main) / st.finish(main)
     dev_src = [torch.as_tensor(t, device=d) for t in host_src]
@@ -387,7 +387,7 @@ def run_kvx(args):
     def run_unit(u):
         w, lo, hi, chunk = u
         if role.role == "decode":
-            st.recv(dev_dst[w], lo, hi, chunk, args.layers_per_chunk)
+            st.recv(dev_dst[w], lo, hi, chunk, args.layers_per_chunk, src_table=dev_src[w])
         else:
             st.send(dev_src[w], dev_dst[w], lo, hi, chunk, args.layers_per_chunk)
 
@@ -508,14 +508,15 @@ def run_kvx(args):
     if ksum and ksum["launches"]:
         kname = "copy_tma_kernel" if args.copy_impl == "tma" else "copy_lsu_kernel"
         achieved = ksum["avg_algorithmic_bytes"] / (kavg / 1e3) / GB
-        if mode == "peer_fused":
+        if mode in ("peer_fused", "peer_pull"):
             bound, peak, pk_src = "nvlink", link_gbs, ("measured in this run: 1 GiB copy-engine "
                                                        "peer copy, slowest pair")
         else:
             bound, peak = "hbm", peaks["hbm_gbs"]
             pk_src = f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"
         role_kernel = {"local_fused": "fused paged copy", "local_staged": "gather",
-                       "peer_ce": "gather (prefill GPU)", "peer_fused": "peer paged copy"}
+                       "peer_ce": "gather (prefill GPU)", "peer_fused": "peer paged copy",
+                       "peer_pull": "paged copy pulling from the prefill GPU"}
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname,
                 "launch_role": role_kernel.get(mode), "avg_launch_ms": kavg,

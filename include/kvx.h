@@ -271,7 +271,9 @@ enum {
   KVX_STREAM_LOCAL_FUSED = 0,  /* one GPU: paged -> paged copy kernel */
   KVX_STREAM_LOCAL_STAGED = 1, /* one GPU: gather -> ring -> scatter */
   KVX_STREAM_PEER_FUSED = 2,   /* sender kernel stores into the receiver's pool */
-  KVX_STREAM_PEER_CE = 3       /* gather -> copy engine P2P -> scatter on the receiver */
+  KVX_STREAM_PEER_CE = 3,      /* gather -> copy engine P2P -> scatter on the receiver */
+  KVX_STREAM_PEER_PULL = 4     /* receiver kernel loads the sender's pool (IPC view) over
+                                  NVLink and stores locally; the prefill GPU's SMs stay free */
 };
 enum { KVX_ROLE_LOCAL = 0, KVX_ROLE_SENDER = 1, KVX_ROLE_RECEIVER = 2 };
 
@@ -299,9 +301,10 @@ void* kvx_streamer_stream(kvx_streamer* s);
 int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t* d_dst_table,
                       int64_t n, int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
                       int32_t layers_per_chunk);
-/* Receiver: the matching units (same n / chunking / layer ranges). */
-int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_dst_table, int64_t n,
-                      int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
+/* Receiver: the matching units (same n / chunking / layer ranges); the source
+ * table is read only by PEER_PULL (the receiver copies from the sender's pool). */
+int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t* d_dst_table,
+                      int64_t n, int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
                       int32_t layers_per_chunk);
 /* End of a step; if stream != NULL it then waits for all queued work. */
 int kvx_streamer_finish(kvx_streamer* s, void* stream);

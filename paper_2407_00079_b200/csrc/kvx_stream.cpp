@@ -14,6 +14,9 @@
 //   LOCAL_FUSED   one GPU: paged->paged copy kernel per unit
 //   LOCAL_STAGED  one GPU: gather -> ring slot -> scatter (two streams)
 //   PEER_FUSED    sender kernel stores straight into the receiver's pool (IPC view)
+//   PEER_PULL     receiver kernel loads the sender's pool (IPC view) over NVLink
+//                 and stores into its own pool; per-unit readiness flags from the
+//                 sender; the prefill GPU's SMs stay free
 //   PEER_CE       sender gathers into a ring slot, the copy engine moves it into
 //                 the receiver's ring (IPC), the receiver scatters; 64-bit flags
 //                 written with stream memory operations order the three queues
@@ -94,7 +97,8 @@ int timed_launch(kvx_streamer* s, cudaStream_t st, double bytes, F&& launch) {
 }
 
 bool is_peer(const kvx_streamer* s) {
-  return s->d.mode == KVX_STREAM_PEER_FUSED || s->d.mode == KVX_STREAM_PEER_CE;
+  return s->d.mode == KVX_STREAM_PEER_FUSED || s->d.mode == KVX_STREAM_PEER_CE ||
+         s->d.mode == KVX_STREAM_PEER_PULL;
 }
 
 struct ExportBlob {
@@ -117,7 +121,7 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
                         kvx_streamer** out) {
   KVX_REQUIRE(desc && out, "kvx_streamer_create: NULL argument");
   const int mode = desc->mode, role = desc->role;
-  KVX_REQUIRE(mode >= KVX_STREAM_LOCAL_FUSED && mode <= KVX_STREAM_PEER_CE,
+  KVX_REQUIRE(mode >= KVX_STREAM_LOCAL_FUSED && mode <= KVX_STREAM_PEER_PULL,
               "kvx_streamer_create: bad mode");
   const bool local = mode == KVX_STREAM_LOCAL_FUSED || mode == KVX_STREAM_LOCAL_STAGED;
   KVX_REQUIRE(local == (role == KVX_ROLE_LOCAL), "kvx_streamer_create: mode/role mismatch");
@@ -219,6 +223,11 @@ int kvx_streamer_export(kvx_streamer* s, uint8_t* blob, int64_t cap, int64_t* le
     if (rc) return rc;
     b.has_pool = 1;
   }
+  if (s->d.role == KVX_ROLE_SENDER && s->d.mode == KVX_STREAM_PEER_PULL) {
+    rc = kvx_ipc_export(kvx_pool_base(s->src), b.pool);
+    if (rc) return rc;
+    b.has_pool = 1;
+  }
   std::memcpy(blob, &b, sizeof(b));
   for (size_t i = 0; i < s->ring.size(); ++i) {
     rc = kvx_ipc_export(s->ring[i], blob + sizeof(b) + i * KVX_IPC_HANDLE_BYTES);
@@ -239,7 +248,9 @@ int kvx_streamer_connect(kvx_streamer* s, const uint8_t* blob, int64_t len,
   int rc = kvx_ipc_open(b.flag, s->device, &p);
   if (rc) return rc;
   s->peer_flag = static_cast<uint64_t*>(p);
-  if (s->d.role == KVX_ROLE_SENDER && s->d.mode == KVX_STREAM_PEER_FUSED) {
+  const bool maps_pool = (s->d.role == KVX_ROLE_SENDER && s->d.mode == KVX_STREAM_PEER_FUSED) ||
+                         (s->d.role == KVX_ROLE_RECEIVER && s->d.mode == KVX_STREAM_PEER_PULL);
+  if (maps_pool) {
     KVX_REQUIRE(b.has_pool && peer_pool, "kvx_streamer_connect: peer pool missing");
     rc = kvx_ipc_open(b.pool, s->device, &p);
     if (rc) return rc;
@@ -272,7 +283,7 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
   KVX_REQUIRE(s && s->d.role != KVX_ROLE_RECEIVER, "kvx_streamer_send: not a sender");
   KVX_REQUIRE(n >= 0 && chunk_blocks >= 1 && layers_per_chunk >= 1 && layer_lo <= layer_hi,
               "kvx_streamer_send: bad ranges");
-  const bool needs_dst = s->d.mode != KVX_STREAM_PEER_CE;
+  const bool needs_dst = s->d.mode != KVX_STREAM_PEER_CE && s->d.mode != KVX_STREAM_PEER_PULL;
   KVX_REQUIRE(d_src_table && (!needs_dst || d_dst_table), "kvx_streamer_send: NULL table");
   kvx::DeviceGuard g(s->device);
   const int64_t slab = kvx_pool_slab_bytes(s->src);
@@ -290,6 +301,12 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
             return kvx_copy_paged(s->src, d_src_table + b0, s->dst, d_dst_table + b0, nb, l0, l1,
                                   s->s_main);
           });
+          break;
+        case KVX_STREAM_PEER_PULL:
+          // the KV of unit c is in the pool once the work queued so far on the
+          // sender's queue (the prefill of that layer, in a serving engine) is done
+          KVX_REQUIRE(s->peer_flag, "kvx_streamer_send: not connected");
+          rc = kvx_signal_write(s->s_main, s->peer_flag, c + 1);
           break;
         case KVX_STREAM_PEER_FUSED:
           KVX_REQUIRE(s->peer_view, "kvx_streamer_send: not connected");
@@ -344,8 +361,8 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
   return KVX_OK;
 }
 
-int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_dst_table, int64_t n,
-                      int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
+int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t* d_dst_table,
+                      int64_t n, int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
                       int32_t layers_per_chunk) {
   KVX_REQUIRE(s && s->d.role == KVX_ROLE_RECEIVER, "kvx_streamer_recv: not a receiver");
   KVX_REQUIRE(n >= 0 && chunk_blocks >= 1 && layers_per_chunk >= 1 && layer_lo <= layer_hi,
@@ -359,8 +376,19 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_dst_table, int64_t n,
       const int32_t l1 = std::min(layer_hi, l0 + layers_per_chunk);
       const int64_t payload = static_cast<int64_t>(l1 - l0) * 2 * nb * slab;
       const uint64_t c = s->seq++;
-      if (s->d.mode != KVX_STREAM_PEER_CE) continue;  // PEER_FUSED: bytes land without us
+      if (s->d.mode == KVX_STREAM_PEER_FUSED) continue;  // bytes land without us
       KVX_REQUIRE(d_dst_table, "kvx_streamer_recv: NULL table");
+      if (s->d.mode == KVX_STREAM_PEER_PULL) {
+        KVX_REQUIRE(d_src_table && s->peer_view, "kvx_streamer_recv: pull needs the src table");
+        int rc = kvx_signal_wait(s->s_main, s->flag, c + 1);  // sender: unit c is ready
+        if (rc) return rc;
+        rc = timed_launch(s, s->s_main, 1.0 * payload, [&] {
+          return kvx_copy_paged(s->peer_view, d_src_table + b0, s->dst, d_dst_table + b0, nb, l0,
+                                l1, s->s_main);
+        });
+        if (rc) return rc;
+        continue;
+      }
       const int slot = static_cast<int>(c % R);
       int rc = kvx_signal_wait(s->s_main, s->flag, c + 1);
       if (rc) return rc;
@@ -383,6 +411,11 @@ int kvx_streamer_finish(kvx_streamer* s, void* stream) {
   if (s->d.mode == KVX_STREAM_PEER_FUSED) {
     int rc = s->d.role == KVX_ROLE_SENDER ? kvx_signal_write(s->s_main, s->peer_flag, s->seq)
                                           : kvx_signal_wait(s->s_main, s->flag, s->seq);
+    if (rc) return rc;
+  }
+  if (s->d.mode == KVX_STREAM_PEER_PULL) {  // receiver -> sender: source blocks consumed
+    int rc = s->d.role == KVX_ROLE_RECEIVER ? kvx_signal_write(s->s_main, s->peer_flag, s->seq)
+                                            : kvx_signal_wait(s->s_main, s->flag, s->seq);
     if (rc) return rc;
   }
   if (stream) {

@@ -10,7 +10,7 @@ chunked-pipeline KV production (proj/src/perf_model.cpp:87-110), the
 per-sender FIFO (proj/src/sim_engine.cpp:409-411).
 
 Modes: ``local_fused`` / ``local_staged`` (N = 1), ``peer_fused`` /
-``peer_ce`` (a prefill GPU and a decode GPU, one process each),
+``peer_ce`` / ``peer_pull`` (a prefill GPU and a decode GPU, one process each),
 ``peer_nccl`` (comparison).
 """
 from __future__ import annotations
@@ -23,7 +23,7 @@ import torch
 from . import kvx
 from .kvx import _L, _i64, _vp, check
 
-MODES = {"local_fused": 0, "local_staged": 1, "peer_fused": 2, "peer_ce": 3}
+MODES = {"local_fused": 0, "local_staged": 1, "peer_fused": 2, "peer_ce": 3, "peer_pull": 4}
 ROLES = {"local": 0, "sender": 1, "receiver": 2}
 
 
@@ -44,7 +44,7 @@ _sig("kvx_streamer_export", C.c_int, _vp, _vp, _i64, C.POINTER(_i64))
 _sig("kvx_streamer_connect", C.c_int, _vp, _vp, _i64, C.POINTER(kvx.KvxPoolDesc))
 _sig("kvx_streamer_stream", _vp, _vp)
 _sig("kvx_streamer_send", C.c_int, _vp, _vp, _vp, _i64, _i64, C.c_int32, C.c_int32, C.c_int32)
-_sig("kvx_streamer_recv", C.c_int, _vp, _vp, _i64, _i64, C.c_int32, C.c_int32, C.c_int32)
+_sig("kvx_streamer_recv", C.c_int, _vp, _vp, _vp, _i64, _i64, C.c_int32, C.c_int32, C.c_int32)
 _sig("kvx_streamer_finish", C.c_int, _vp, _vp)
 _sig("kvx_streamer_after", C.c_int, _vp, _vp)
 _sig("kvx_streamer_set_timing", C.c_int, _vp, C.c_int, C.c_int)
@@ -102,10 +102,11 @@ class Streamer:
                                    layers_per_chunk))
 
     def recv(self, dst_table: torch.Tensor, layer_lo: int, layer_hi: int, chunk_blocks: int = 0,
-             layers_per_chunk: int = 1):
+             layers_per_chunk: int = 1, src_table: Optional[torch.Tensor] = None):
         n = dst_table.numel()
-        check(_L.kvx_streamer_recv(self.h, dst_table.data_ptr(), n, chunk_blocks or max(n, 1),
-                                   layer_lo, layer_hi, layers_per_chunk))
+        check(_L.kvx_streamer_recv(self.h, src_table.data_ptr() if src_table is not None else None,
+                                   dst_table.data_ptr(), n, chunk_blocks or max(n, 1), layer_lo,
+                                   layer_hi, layers_per_chunk))
 
     def finish(self, stream=None):
         check(_L.kvx_streamer_finish(self.h, kvx._stream(stream) if stream is not None else None))
@@ -164,7 +165,8 @@ class NcclStreamer:
                     self.ring[slot].tensor()[:payload], self.peer)
             self.c += 1
 
-    def recv(self, dst_table, layer_lo, layer_hi, chunk_blocks=0, layers_per_chunk=1):
+    def recv(self, dst_table, layer_lo, layer_hi, chunk_blocks=0, layers_per_chunk=1,
+             src_table=None):
         for b0, nb, l0, l1 in self._units(dst_table.numel(), chunk_blocks, layer_lo, layer_hi,
                                           layers_per_chunk):
             slot = self.c % len(self.ring)
