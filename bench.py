@@ -453,7 +453,11 @@ def run_kvx(args):
     launches_all = int(sum_over_ranks(float(launches), d))
     payload = plan["payload_total"]
     value = payload * args.steps / (ms_total / 1e3) / GB
-    kavg = max_over_ranks(ksum["avg_ms"] if ksum and ksum["launches"] else 0.0, d)
+    # the dominant kernel may run on either end of a pair (pull: the decode GPU)
+    has_k = bool(ksum and ksum["launches"])
+    kavg = max_over_ranks(ksum["avg_ms"] if has_k else 0.0, d)
+    kbytes = max_over_ranks(ksum["avg_algorithmic_bytes"] if has_k else 0.0, d)
+    klaunches = int(sum_over_ranks(float(ksum["launches"]) if has_k else 0.0, d))
 
     # ---- e2e: public API with HOST block tables every step (pinned H2D on the
     # streamer queue), completion word D2H after the step
@@ -505,9 +509,9 @@ def run_kvx(args):
 
     peaks = measured_peaks()
     roof = None
-    if ksum and ksum["launches"]:
+    if klaunches:
         kname = "copy_tma_kernel" if args.copy_impl == "tma" else "copy_lsu_kernel"
-        achieved = ksum["avg_algorithmic_bytes"] / (kavg / 1e3) / GB
+        achieved = kbytes / (kavg / 1e3) / GB
         if mode in ("peer_fused", "peer_pull"):
             bound, peak, pk_src = "nvlink", link_gbs, ("measured in this run: 1 GiB copy-engine "
                                                        "peer copy, slowest pair")
@@ -520,8 +524,8 @@ def run_kvx(args):
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(kname), "kernel": kname,
                 "launch_role": role_kernel.get(mode), "avg_launch_ms": kavg,
-                "launches_timed": ksum["launches"],
-                "algorithmic_bytes_per_launch": ksum["avg_algorithmic_bytes"],
+                "launches_timed": klaunches,
+                "algorithmic_bytes_per_launch": kbytes,
                 "peak_source": pk_src}
 
     if rank == 0:
