@@ -68,7 +68,7 @@ def _torchrun(n, *args, timeout=900):
 
 
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("mode", ["peer_ce", "peer_fused", "peer_nccl"])
+@pytest.mark.parametrize("mode", ["peer_ce", "peer_fused", "peer_pull", "peer_nccl"])
 def test_two_gpu_modes_bit_exact(mode):
     d = _torchrun(2, "--mode", mode, "--requests", "4", "--wave", "2", "--steps", "2",
                   "--warmup", "3", "--no-match", "--no-e2e", "--no-cpu-baseline")
