@@ -14,7 +14,8 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from .kvx import KvxError, ValidationError, KVX_EINVAL, KVX_OK
+from .kvx import KVX_EINVAL, KVX_OK, KvxError, ValidationError
+from .kvx import alive as _kvx_alive
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libkvcsim_gpu.so")
@@ -76,7 +77,7 @@ class CachePool:
         self.policy = policy
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _kvx_alive():
             _L.kvcsim_pool_destroy(self.h)
             self.h = None
 

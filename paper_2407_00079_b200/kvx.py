@@ -26,6 +26,7 @@ streams); all compute runs in libkvx's sm_100a kernels.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 from typing import Optional, Sequence
@@ -41,6 +42,23 @@ if not os.path.exists(LIB_PATH):
         "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
 
 _L = C.CDLL(LIB_PATH)
+
+# Handles are released by __del__; at interpreter exit module globals are torn
+# down in arbitrary order, so releases after exit starts are skipped (the
+# process exit frees the device memory anyway).
+_ALIVE = True
+
+
+def _mark_exit():
+    global _ALIVE
+    _ALIVE = False
+
+
+atexit.register(_mark_exit)
+
+
+def alive() -> bool:
+    return _ALIVE is True
 
 KVX_OK, KVX_EINVAL, KVX_ENOMEM, KVX_ECUDA, KVX_EABORTED, KVX_EAGAIN = range(6)
 KEY_EMPTY = -(1 << 63)
@@ -220,7 +238,7 @@ class BlockIndex:
         self.device = device
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _ALIVE is True:
             _L.kvx_index_destroy(self.h)
             self.h = None
 
@@ -323,7 +341,7 @@ class KVPool:
         self.base = int(_L.kvx_pool_base(h))
 
     def close(self):
-        if getattr(self, "h", None) and getattr(self, "owned", True):
+        if getattr(self, "h", None) and getattr(self, "owned", True) and _ALIVE is True:
             _L.kvx_pool_destroy(self.h)
             self.h = None
 
@@ -392,7 +410,7 @@ class TransferEngine:
         self.stream_handle = int(_L.kvx_xfer_stream(h))
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _ALIVE is True:
             _L.kvx_xfer_destroy(self.h)
             self.h = None
 
@@ -458,7 +476,7 @@ class DeviceBuffer:
         self.device = device
 
     def close(self):
-        if getattr(self, "ptr", 0):
+        if getattr(self, "ptr", 0) and _ALIVE is True:
             _L.kvx_device_free(self.device, _vp(self.ptr))
             self.ptr = 0
 
@@ -479,7 +497,7 @@ class SlotAllocator:
         self.slots = slots
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and _ALIVE is True:
             _L.kvx_slot_alloc_destroy(self.h)
             self.h = None
 

@@ -55,7 +55,7 @@ class KVStore:
         p.owned = False  # the store owns the pool
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and kvx.alive():
             _L.kvx_store_destroy(self.h)
             self.h = None
 

@@ -71,7 +71,7 @@ class Streamer:
                                                 device=self.device)
 
     def close(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and kvx.alive():
             _L.kvx_streamer_destroy(self.h)
             self.h = None
 

@@ -23,9 +23,9 @@ GB = 1e9
 
 
 def timed(fn, reps=3):
+    """Local timing only -- callers keep the collective calls symmetric."""
     fn()
     torch.cuda.synchronize()
-    dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s = torch.cuda.current_stream()
     e0.record(s)
