@@ -55,8 +55,7 @@ def parse_args():
                     help="layers per streamed unit; 0 = auto (1 for config 2, whose units are "
                          "512 MiB per layer; 16 for config 3, whose 2048-token chunks are only "
                          "8 MiB per layer and launch-overhead bound one layer at a time)")
-    ap.add_argument("--ring", type=int, default=4,
-                    help="staging slots per end (even: the copy-engine sender runs 2 lanes)")
+    ap.add_argument("--ring", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3],
                     help="1: one 8K request; 2: 64 x 8K requests, 50%% shared prefix "
                          "(default); 3: one 128K request")

@@ -42,8 +42,10 @@ struct kvx_streamer {
   int device = 0;
   cudaStream_t s_main = nullptr;     // gather / fused copy (sender, local) or scatter (receiver)
   cudaStream_t s_second = nullptr;   // LOCAL_STAGED scatter stream
+  kvx_xfer* xfer = nullptr;          // PEER_CE copy queue
   std::vector<void*> ring;           // local staging slots (cudaMalloc, IPC-exportable)
   std::vector<void*> peer_ring;      // receiver's slots as mapped on the sender
+  std::vector<uint64_t> slot_ticket; // PEER_CE: copy that last read each gather slot
   std::vector<cudaEvent_t> slot_ev;  // LOCAL_STAGED: scatter that last read each slot
   std::vector<cudaEvent_t> gather_ev;
   uint64_t* flag = nullptr;          // local 64-bit flag word (peer writes it)
@@ -127,8 +129,8 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
   KVX_REQUIRE(role != KVX_ROLE_SENDER || src, "sender needs a src pool");
   KVX_REQUIRE(role != KVX_ROLE_RECEIVER || dst, "receiver needs a dst pool");
   const bool staged = mode == KVX_STREAM_LOCAL_STAGED || mode == KVX_STREAM_PEER_CE;
-  KVX_REQUIRE(!staged || (desc->ring >= 1 && desc->ring <= 32 && desc->slot_bytes > 0),
-              "staged modes need 1 <= ring <= 32 and slot_bytes > 0");
+  KVX_REQUIRE(!staged || (desc->ring >= 1 && desc->slot_bytes > 0),
+              "staged modes need ring >= 1 and slot_bytes > 0");
   auto* s = new kvx_streamer();
   s->d = *desc;
   s->src = src;
@@ -142,10 +144,7 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
   };
   cudaError_t e = cudaStreamCreateWithFlags(&s->s_main, cudaStreamNonBlocking);
   if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: stream"));
-  // LOCAL_STAGED: scatter stream.  PEER_CE sender: second lane (units alternate
-  // between two in-order queues) when the ring size is even.
-  if (mode == KVX_STREAM_LOCAL_STAGED ||
-      (mode == KVX_STREAM_PEER_CE && role == KVX_ROLE_SENDER && desc->ring % 2 == 0)) {
+  if (mode == KVX_STREAM_LOCAL_STAGED) {
     e = cudaStreamCreateWithFlags(&s->s_second, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: stream"));
   }
@@ -161,12 +160,17 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
       s->slot_ev.push_back(ev1);
       s->gather_ev.push_back(ev2);
     }
+    s->slot_ticket.assign(desc->ring, 0);
   }
   if (is_peer(s)) {
     e = cudaMalloc(reinterpret_cast<void**>(&s->flag), 256);
     if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: flag"));
     cudaMemset(s->flag, 0, 256);
     cudaDeviceSynchronize();
+  }
+  if (mode == KVX_STREAM_PEER_CE && role == KVX_ROLE_SENDER) {
+    int rc = kvx_xfer_create(s->device, &s->xfer);
+    if (rc) return fail(rc);
   }
   *out = s;
   return KVX_OK;
@@ -177,6 +181,7 @@ int kvx_streamer_destroy(kvx_streamer* s) {
   kvx::DeviceGuard g(s->device);
   if (s->s_main) cudaStreamSynchronize(s->s_main);
   if (s->s_second) cudaStreamSynchronize(s->s_second);
+  if (s->xfer) kvx_xfer_destroy(s->xfer);
   for (void* p : s->peer_ring) kvx_ipc_close(p);
   if (s->peer_flag) kvx_ipc_close(s->peer_flag);
   if (s->peer_view) {
@@ -326,27 +331,25 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
           break;
         }
         case KVX_STREAM_PEER_CE: {
-          // Unit c runs on lane c % lanes as [gather -> wait until the receiver
-          // drained slot c % R (unit c - R) -> copy-engine copy -> flag].  With
-          // R a multiple of the lane count a slot is always reused on the same
-          // lane, so stream order protects the local gather slot; per-slot flags
-          // stay monotone although the two lanes finish out of order.  Four API
-          // calls per unit keep 8 MiB units link-bound rather than host-bound.
           KVX_REQUIRE(!s->peer_ring.empty(), "kvx_streamer_send: not connected");
           KVX_REQUIRE(payload <= s->d.slot_bytes, "kvx_streamer_send: unit larger than a slot");
           const int slot = static_cast<int>(c % R);
-          cudaStream_t lane = (s->s_second && (c & 1)) ? s->s_second : s->s_main;
-          rc = timed_launch(s, lane, 2.0 * payload, [&] {
-            return kvx_gather(s->src, d_src_table + b0, nb, l0, l1, s->ring[slot], lane);
-          });
-          if (rc) return rc;
-          if (c >= static_cast<uint64_t>(R)) {
-            rc = kvx_signal_wait(lane, s->flag + slot, c - R + 1);
+          if (s->slot_ticket[slot]) {  // the copy that last read this gather slot
+            rc = kvx_transfer_wait_stream(s->xfer, s->slot_ticket[slot], s->s_main);
             if (rc) return rc;
           }
-          KVX_CUDA(cudaMemcpyAsync(s->peer_ring[slot], s->ring[slot], static_cast<size_t>(payload),
-                                   cudaMemcpyDefault, lane));
-          rc = kvx_signal_write(lane, s->peer_flag + slot, c + 1);  // unit c landed
+          rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
+            return kvx_gather(s->src, d_src_table + b0, nb, l0, l1, s->ring[slot], s->s_main);
+          });
+          if (rc) return rc;
+          if (c >= static_cast<uint64_t>(R)) {  // receiver drained its slot (unit c - R)
+            rc = kvx_signal_wait(kvx_xfer_stream(s->xfer), s->flag, c - R + 1);
+            if (rc) return rc;
+          }
+          rc = kvx_transfer_submit(s->xfer, s->peer_ring[slot], s->ring[slot], payload, s->s_main,
+                                   &s->slot_ticket[slot]);
+          if (rc) return rc;
+          rc = kvx_transfer_signal(s->xfer, s->peer_flag, c + 1);  // unit c landed
           break;
         }
         default:
@@ -387,13 +390,13 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t
         continue;
       }
       const int slot = static_cast<int>(c % R);
-      int rc = kvx_signal_wait(s->s_main, s->flag + slot, c + 1);  // unit c landed in the slot
+      int rc = kvx_signal_wait(s->s_main, s->flag, c + 1);
       if (rc) return rc;
       rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
         return kvx_scatter(s->dst, d_dst_table + b0, nb, l0, l1, s->ring[slot], s->s_main);
       });
       if (rc) return rc;
-      rc = kvx_signal_write(s->s_main, s->peer_flag + slot, c + 1);  // slot drained
+      rc = kvx_signal_write(s->s_main, s->peer_flag, c + 1);  // slot drained
       if (rc) return rc;
     }
   }
@@ -420,6 +423,7 @@ int kvx_streamer_finish(kvx_streamer* s, void* stream) {
     KVX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     std::vector<cudaStream_t> qs = {s->s_main};
     if (s->s_second) qs.push_back(s->s_second);
+    if (s->xfer) qs.push_back(as_stream(kvx_xfer_stream(s->xfer)));
     for (cudaStream_t q : qs) {
       KVX_CUDA(cudaEventRecord(ev, q));
       KVX_CUDA(cudaStreamWaitEvent(as_stream(stream), ev, 0));
@@ -438,6 +442,7 @@ int kvx_streamer_after(kvx_streamer* s, void* stream) {
   KVX_CUDA(cudaEventRecord(ev, as_stream(stream)));
   KVX_CUDA(cudaStreamWaitEvent(s->s_main, ev, 0));
   if (s->s_second) KVX_CUDA(cudaStreamWaitEvent(s->s_second, ev, 0));
+  if (s->xfer) KVX_CUDA(cudaStreamWaitEvent(as_stream(kvx_xfer_stream(s->xfer)), ev, 0));
   KVX_CUDA(cudaEventDestroy(ev));
   return KVX_OK;
 }
