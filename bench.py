@@ -337,7 +337,10 @@ def run_kvx(args):
 
     mode = args.mode
     if mode == "auto":
-        mode = "local_fused" if role.role == "local" else "peer_ce"
+        # measured best per config (profiles/r01): copy engines for Config 2's
+        # 512 MiB units, the decode GPU pulling for Config 3's 128 MiB units
+        mode = ("local_fused" if role.role == "local" else
+                "peer_pull" if args.config == 3 else "peer_ce")
     if (role.role == "local") != mode.startswith("local"):
         raise SystemExit(f"mode {mode} does not fit {world} GPU(s)")
 
