@@ -428,9 +428,10 @@ def run_kvx(args):
         raise SystemExit(f"PARITY FAILURE: {bad} mismatched 64-bit words")
 
     # ---- timed region: CUDA events on the streamer's queue, max over ranks
-    # time a sample of the dominant launches: every launch when units are large,
-    # every 16th when they are small (an event pair costs ~µs of host time)
-    st.set_timing(True, 16 if args.config == 3 else 1)
+    # time a sample of the dominant launches -- every 4th (every 16th for the
+    # small Config 3 units): an event pair costs ~µs of host time and sits in
+    # the timed region
+    st.set_timing(True, 16 if args.config == 3 else 4)
     st.launch_stats(reset=True)
     clocks = ClockSampler(dev)
     clocks.start()
