@@ -93,6 +93,68 @@ __global__ void __launch_bounds__(kLsuThreads) copy_lsu_kernel(const SlabCopy c)
   }
 }
 
+__device__ __forceinline__ void st_stream(int4* p, const int4& v) {
+  asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Variant of copy_lsu_kernel with evict-first (.cs) stores and the next work
+// item's loads issued before the current item's stores (8 x 16 B in flight per
+// thread).  Selected with KVX_LSU_VARIANT for measurement.
+template <bool kCsStores, bool kPipelined>
+__global__ void __launch_bounds__(kLsuThreads) copy_lsu_v_kernel(const SlabCopy c) {
+  const int64_t parts = (c.slab + kLsuItem - 1) / kLsuItem;
+  const int64_t items = c.planes * c.n * parts;
+  int4 r[kLsuUnroll];
+  int nv = 0;
+  int4* dv = nullptr;
+  auto load = [&](int64_t it, int4 (&buf)[kLsuUnroll], int& n, int4*& dst) {
+    const int64_t u = it / parts;
+    const int64_t off = (it - u * parts) * kLsuItem;
+    const uint8_t* s;
+    uint8_t* d;
+    unit_addrs(c, u, s, d);
+    n = static_cast<int>(min(kLsuItem, c.slab - off) >> 4);
+    const int4* sv = reinterpret_cast<const int4*>(s + off);
+    dst = reinterpret_cast<int4*>(d + off);
+#pragma unroll
+    for (int j = 0; j < kLsuUnroll; ++j) {
+      const int v = threadIdx.x + j * kLsuThreads;
+      if (v < n) buf[j] = ld_stream(sv + v);
+    }
+  };
+  auto store = [&](const int4 (&buf)[kLsuUnroll], int n, int4* dst) {
+#pragma unroll
+    for (int j = 0; j < kLsuUnroll; ++j) {
+      const int v = threadIdx.x + j * kLsuThreads;
+      if (v < n) {
+        if (kCsStores) st_stream(dst + v, buf[j]);
+        else dst[v] = buf[j];
+      }
+    }
+  };
+  int64_t it = blockIdx.x;
+  if (it >= items) return;
+  load(it, r, nv, dv);
+  for (; it < items; it += gridDim.x) {
+    if (kPipelined && it + gridDim.x < items) {
+      int4 r2[kLsuUnroll];
+      int nv2;
+      int4* dv2;
+      load(it + gridDim.x, r2, nv2, dv2);
+      store(r, nv, dv);
+#pragma unroll
+      for (int j = 0; j < kLsuUnroll; ++j) r[j] = r2[j];
+      nv = nv2;
+      dv = dv2;
+    } else {
+      store(r, nv, dv);
+      if (it + gridDim.x < items) load(it + gridDim.x, r, nv, dv);
+    }
+  }
+}
+
 // ---- TMA bulk-copy pipeline ----------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -247,7 +309,16 @@ int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
     const int64_t items = units * ((c.slab + kLsuItem - 1) / kLsuItem);
     const int blocks =
         static_cast<int>(std::min<int64_t>(items, static_cast<int64_t>(sms) * ctas_per_sm));
-    copy_lsu_kernel<<<blocks, kLsuThreads, 0, s>>>(c);
+    static const int variant = [] {
+      const char* e = std::getenv("KVX_LSU_VARIANT");  // measurement knob
+      return e ? std::atoi(e) : 0;
+    }();
+    switch (variant) {
+      case 1: copy_lsu_v_kernel<true, false><<<blocks, kLsuThreads, 0, s>>>(c); break;
+      case 2: copy_lsu_v_kernel<false, true><<<blocks, kLsuThreads, 0, s>>>(c); break;
+      case 3: copy_lsu_v_kernel<true, true><<<blocks, kLsuThreads, 0, s>>>(c); break;
+      default: copy_lsu_kernel<<<blocks, kLsuThreads, 0, s>>>(c); break;
+    }
     KVX_LAUNCH_CHECK("copy_lsu_kernel");
   }
   return KVX_OK;
