@@ -800,9 +800,19 @@ def bench_match(args, dev, rank, world, role):
                               "one prefill instance index per GPU; per-request best combined "
                               "by all-reduce(MAX) over packed (len<<32 | ~id) words (NCCL)")},
         "kernels": {
-            "block_hash_kernel": {"avg_ms": hs["avg_ms"], "bytes": hs["avg_algorithmic_bytes"],
-                                  "achieved_gbs": hash_gbs,
-                                  "frac_hbm": hash_gbs / peaks["hbm_gbs"]},
+            "block_hash_kernel": {
+                "avg_ms": hs["avg_ms"], "bytes": hs["avg_algorithmic_bytes"],
+                "achieved_gbs": hash_gbs, "frac_hbm": hash_gbs / peaks["hbm_gbs"],
+                # the real bound: int64 chain_hash on the ALU pipe (one per token
+                # for contents + one per block for the key fold)
+                "compute_roofline": {
+                    "bound": "alu (64-bit chain_hash emulated on 32-bit pipes)",
+                    "chain_hashes": int(tok_bytes // 4 + n_blocks),
+                    "achieved_per_s": (tok_bytes // 4 + n_blocks) / (hs["avg_ms"] / 1e3),
+                    "peak_per_s": 760e9,
+                    "peak_source": "measured: tests/perf/hash_pipe_micro.cu, full-chip, "
+                                   "4 independent chains per thread",
+                    "frac": (tok_bytes // 4 + n_blocks) / (hs["avg_ms"] / 1e3) / 760e9}},
             "match_kernel": {"avg_ms": ms_match["avg_ms"], "probes": n_probes,
                              "bytes": match_bytes, "achieved_gbs": match_gbs,
                              "frac_hbm": match_gbs / peaks["hbm_gbs"],
