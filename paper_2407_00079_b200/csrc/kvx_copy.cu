@@ -160,7 +160,7 @@ __device__ __forceinline__ void lsu_copy(const SlabCopy& c) {
   }
 }
 
-__global__ void __launch_bounds__(kLsuThreads) copy_lsu_kernel(const SlabCopy c) {
+__global__ void __launch_bounds__(kLsuThreads, 2) copy_lsu_kernel(const SlabCopy c) {
   lsu_copy<true, true>(c);
 }
 
