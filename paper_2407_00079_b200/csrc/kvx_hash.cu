@@ -195,7 +195,10 @@ __device__ __forceinline__ void fold_requests(const int64_t* __restrict__ key_of
 // at its dependency latency, four per sub-partition would be issue bound);
 // other CTAs on those SMs exit.  Every other warp produces contents, then
 // joins the folding of whatever is still unclaimed.
-constexpr int kFoldWarps = 4;
+#ifndef KVX_HASH_FOLD_WARPS
+#define KVX_HASH_FOLD_WARPS 4
+#endif
+constexpr int kFoldWarps = KVX_HASH_FOLD_WARPS;
 
 __global__ void __launch_bounds__(kHashThreads, KVX_HASH_MIN_CTAS) block_hash_fused_kernel(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
