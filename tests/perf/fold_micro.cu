@@ -4,6 +4,8 @@
 //   b) same, loads only (no stores)
 //   c) warp = 32 requests, 32-block windows transposed through shared memory
 //      (coalesced 256-byte rows in, coalesced rows out)
+//   d) the chain alone (contents in registers)   e) two requests per lane
+//   f) 256-bit loads/stores, 8 or 16 entries per batch, 1 or 4 warps per SM
 #include <cstdio>
 #include <vector>
 
@@ -60,6 +62,83 @@ __global__ void fold_transposed(const int64_t* key_off, int64_t* keys, int n_req
   (void)my_n;
 }
 
+// d) the chain alone: contents from registers (no memory in the loop)
+__global__ void fold_regs(const int64_t* key_off, int64_t* keys, int n_req) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_req) return;
+  const int64_t k0 = key_off[r], k1 = key_off[r + 1];
+  int64_t c[16];
+  for (int j = 0; j < 16; ++j) c[j] = keys[k0 + j];
+  int64_t prev = 0;
+  for (int64_t k = k0; k < k1; k += 16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) prev = kvx::chain_hash(prev, static_cast<uint64_t>(c[j]));
+  }
+  keys[k0] = prev;
+}
+
+// e) two requests per lane, chained interleaved (loads one batch ahead, stores)
+__global__ void fold_two(const int64_t* key_off, int64_t* keys, int n_req) {
+  const int r = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (r + 1 >= n_req + 1) return;
+  const int64_t a0 = key_off[r], a1 = key_off[r + 1], b0 = key_off[r + 1], b1 = key_off[r + 2];
+  const int64_t n = min(a1 - a0, b1 - b0);
+  int64_t pa = 0, pb = 0;
+  int64_t ca[8], cb[8];
+  for (int j = 0; j < 8; ++j) { ca[j] = keys[a0 + j]; cb[j] = keys[b0 + j]; }
+  for (int64_t k = 0; k < n; k += 8) {
+    int64_t na[8], nb[8];
+    for (int j = 0; j < 8; ++j) {
+      na[j] = (k + 8 + j < n) ? keys[a0 + k + 8 + j] : 0;
+      nb[j] = (k + 8 + j < n) ? keys[b0 + k + 8 + j] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      pa = kvx::chain_hash(pa, static_cast<uint64_t>(ca[j]));
+      pb = kvx::chain_hash(pb, static_cast<uint64_t>(cb[j]));
+      keys[a0 + k + j] = pa;
+      keys[b0 + k + j] = pb;
+    }
+    for (int j = 0; j < 8; ++j) { ca[j] = na[j]; cb[j] = nb[j]; }
+  }
+}
+
+// f) lane = request, 256-bit volatile loads one 16-batch ahead, 256-bit stores
+__device__ __forceinline__ void ld4v(const int64_t* p, int64_t* v) {
+  asm volatile("ld.volatile.global.v4.s64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void st4v(int64_t* p, const int64_t* v) {
+  asm volatile("st.global.v4.s64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(v[0]), "l"(v[1]), "l"(v[2]),
+               "l"(v[3]) : "memory");
+}
+template <int B>
+__global__ void fold_vec(const int64_t* key_off, int64_t* keys, int n_req) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n_req) return;
+  const int64_t k0 = key_off[r], k1 = key_off[r + 1];
+  int64_t prev = 0;
+  int64_t c[B];
+  for (int g = 0; g < B / 4; ++g) ld4v(keys + k0 + 4 * g, c + 4 * g);
+  for (int64_t k = k0; k < k1; k += B) {
+    int64_t nx[B];
+    if (k + B < k1) {
+#pragma unroll
+      for (int g = 0; g < B / 4; ++g) ld4v(keys + k + B + 4 * g, nx + 4 * g);
+    }
+    int64_t o[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      prev = kvx::chain_hash(prev, static_cast<uint64_t>(c[j]));
+      o[j] = prev;
+    }
+#pragma unroll
+    for (int g = 0; g < B / 4; ++g) st4v(keys + k + 4 * g, o + 4 * g);
+#pragma unroll
+    for (int j = 0; j < B; ++j) c[j] = nx[j];
+  }
+}
+
 int main() {
   std::vector<int64_t> off(kReq + 1);
   for (int i = 0; i <= kReq; ++i) off[i] = static_cast<int64_t>(i) * kBlk;
@@ -72,17 +151,27 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   float ms;
-  for (int v = 0; v < 3; ++v) {
+  for (int v = 0; v < 10; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       if (v == 0) fold_strided<<<kReq / 32, 32>>>(d_off, d_keys, kReq, 1);
       if (v == 1) fold_strided<<<kReq / 32, 32>>>(d_off, d_keys, kReq, 0);
       if (v == 2) fold_transposed<<<kReq / 32, 32>>>(d_off, d_keys, kReq);
+      if (v == 3) fold_regs<<<kReq / 32, 32>>>(d_off, d_keys, kReq);
+      if (v == 4) fold_two<<<kReq / 64, 32>>>(d_off, d_keys, kReq);
+      if (v == 5) fold_strided<<<kReq / 128, 128>>>(d_off, d_keys, kReq, 1);
+      if (v == 6) fold_vec<8><<<kReq / 32, 32>>>(d_off, d_keys, kReq);
+      if (v == 7) fold_vec<8><<<kReq / 128, 128>>>(d_off, d_keys, kReq);
+      if (v == 8) fold_vec<16><<<kReq / 32, 32>>>(d_off, d_keys, kReq);
+      if (v == 9) fold_vec<16><<<kReq / 128, 128>>>(d_off, d_keys, kReq);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
     }
     cudaEventElapsedTime(&ms, a, b);
-    const char* names[] = {"strided load+store", "strided load only", "smem transposed"};
+    const char* names[] = {"strided load+store", "strided load only", "smem transposed",
+                           "registers only", "2 requests/lane", "a) 4 warps/CTA",
+                           "f) vec8 1 warp/CTA", "f) vec8 4 warps/CTA", "f) vec16 1 warp/CTA",
+                           "f) vec16 4 warps/CTA"};
     std::printf("%-20s %8.1f us  = %.1f cycles/step @1.965GHz\n", names[v], ms * 1e3,
                 ms * 1e-3 * 1.965e9 / kBlk);
   }
