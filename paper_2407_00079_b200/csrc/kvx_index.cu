@@ -401,7 +401,11 @@ int kvx_index_create(int device, int64_t capacity_hint, kvx_index** out) {
     delete x;
     return cuda_error(e, "kvx_index_create: cudaMalloc(counters)");
   }
-  cudaMemset(x->ctr, 0, sizeof(Counters));
+  e = cudaMemsetAsync(x->ctr, 0, sizeof(Counters), nullptr);
+  if (e != cudaSuccess) {
+    kvx_index_destroy(x);
+    return cuda_error(e, "kvx_index_create: cudaMemset(counters)");
+  }
   int64_t slots = next_pow2(static_cast<int64_t>(static_cast<double>(capacity_hint) / kTargetLoad) + 1);
   int st = rebuild(x, slots, nullptr);
   if (st == KVX_OK) {

@@ -94,6 +94,7 @@ struct kvx_xfer {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::vector<cudaEvent_t> ring;  // ticket -> ring[ticket % size]
+  cudaEvent_t dep = nullptr;      // producer-stream dependency of the next submit
   uint64_t next_ticket = 1;
 };
 
@@ -127,6 +128,11 @@ int kvx_xfer_create(int device, kvx_xfer** out) {
     return cuda_error(e, "kvx_xfer_create: cudaStreamCreate");
   }
   x->ring.resize(kTicketRing, nullptr);
+  e = cudaEventCreateWithFlags(&x->dep, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    kvx_xfer_destroy(x);
+    return cuda_error(e, "kvx_xfer_create: cudaEventCreate");
+  }
   for (auto& ev : x->ring) {
     e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     if (e != cudaSuccess) {
@@ -144,6 +150,7 @@ int kvx_xfer_destroy(kvx_xfer* x) {
   if (x->stream) cudaStreamSynchronize(x->stream);
   for (auto ev : x->ring)
     if (ev) cudaEventDestroy(ev);
+  if (x->dep) cudaEventDestroy(x->dep);
   if (x->stream) cudaStreamDestroy(x->stream);
   delete x;
   return KVX_OK;
@@ -159,10 +166,10 @@ int kvx_transfer_submit(kvx_xfer* x, void* dst, const void* src, int64_t bytes,
   DeviceGuard g(x->device);
   if (after_stream) {
     // Order after the producer (e.g. the gather of this layer) without a
-    // host round trip: record on the producer stream, wait on the queue.
-    cudaEvent_t dep = x->ring[x->next_ticket % kTicketRing];
-    KVX_CUDA(cudaEventRecord(dep, as_stream(after_stream)));
-    KVX_CUDA(cudaStreamWaitEvent(x->stream, dep, 0));
+    // host round trip: record on the producer stream, wait on the queue (the
+    // wait captures the event's state, so the event is reusable at once).
+    KVX_CUDA(cudaEventRecord(x->dep, as_stream(after_stream)));
+    KVX_CUDA(cudaStreamWaitEvent(x->stream, x->dep, 0));
   }
   if (bytes > 0)
     KVX_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault, x->stream));

@@ -154,19 +154,21 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
       e = cudaMalloc(&p, static_cast<size_t>(desc->slot_bytes));
       if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: ring"));
       s->ring.push_back(p);
-      cudaEvent_t ev1, ev2;
-      cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming);
-      s->slot_ev.push_back(ev1);
-      s->gather_ev.push_back(ev2);
+      cudaEvent_t ev1 = nullptr, ev2 = nullptr;
+      e = cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming);
+      if (e == cudaSuccess) s->slot_ev.push_back(ev1);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming);
+      if (e == cudaSuccess) s->gather_ev.push_back(ev2);
+      if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: event"));
     }
     s->slot_ticket.assign(desc->ring, 0);
   }
   if (is_peer(s)) {
     e = cudaMalloc(reinterpret_cast<void**>(&s->flag), 256);
     if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: flag"));
-    cudaMemset(s->flag, 0, 256);
-    cudaDeviceSynchronize();
+    e = cudaMemsetAsync(s->flag, 0, 256, s->s_main);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->s_main);  // zero before the peer maps it
+    if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: flag"));
   }
   if (mode == KVX_STREAM_PEER_CE && role == KVX_ROLE_SENDER) {
     int rc = kvx_xfer_create(s->device, &s->xfer);
