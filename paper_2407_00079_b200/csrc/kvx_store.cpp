@@ -17,6 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "kvx.h"
@@ -79,6 +82,32 @@ int insert_host(kvx_store* s, const int64_t* keys, const int64_t* slots, int64_t
   return KVX_OK;
 }
 
+// Bytes of blocks st[i] (source pool) -> dt[i] (destination pool), every
+// layer, K and V, on the source GPU.  Across GPUs of one process the
+// destination pool is reached through UVA once peer access is on: the copy
+// kernel's stores go over NVLink.
+int copy_blocks(kvx_store* src, kvx_store* dst, const std::vector<int32_t>& st,
+                const std::vector<int32_t>& dt) {
+  const int64_t m = static_cast<int64_t>(st.size());
+  if (dst->device != src->device) {
+    int rc = kvx_enable_peer(src->device, dst->device);
+    if (rc) return rc;
+  }
+  kvx::DeviceGuard g(src->device);
+  int rc = ensure_scratch(src, m);
+  if (rc) return rc;
+  int32_t* d_tables = reinterpret_cast<int32_t*>(src->d_scratch);
+  KVX_CUDA(cudaMemcpyAsync(d_tables, st.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice,
+                           src->stream));
+  KVX_CUDA(cudaMemcpyAsync(d_tables + m, dt.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice,
+                           src->stream));
+  rc = kvx_copy_paged(src->pool, d_tables, dst->pool, d_tables + m, m, 0,
+                      kvx_pool_layers(src->pool), src->stream);
+  if (rc) return rc;
+  KVX_CUDA(cudaStreamSynchronize(src->stream));
+  return KVX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -127,23 +156,30 @@ int kvx_store_put(kvx_store* s, const int64_t* h_keys, int64_t n, int32_t* h_slo
   std::vector<int64_t> have;
   int rc = lookup_host(s, h_keys, n, have);
   if (rc) return rc;
+  // absent keys get one slot each, however often they repeat in this call
   std::vector<int64_t> new_keys;
-  std::vector<size_t> pos;
+  std::unordered_map<int64_t, size_t> first;  // absent key -> index in new_keys
+  std::vector<size_t> which(static_cast<size_t>(n), SIZE_MAX);
   for (int64_t i = 0; i < n; ++i) {
     if (have[i] >= 0) {
       h_slots[i] = static_cast<int32_t>(have[i]);
-    } else {
-      new_keys.push_back(h_keys[i]);
-      pos.push_back(static_cast<size_t>(i));
+      continue;
     }
+    auto it = first.emplace(h_keys[i], new_keys.size()).first;
+    if (it->second == new_keys.size()) new_keys.push_back(h_keys[i]);
+    which[i] = it->second;
   }
   std::vector<int32_t> got(new_keys.size());
   rc = kvx_slot_alloc_take(s->alloc, static_cast<int64_t>(new_keys.size()), got.data());
   if (rc) return rc;
   std::vector<int64_t> vals(got.begin(), got.end());
   rc = insert_host(s, new_keys.data(), vals.data(), static_cast<int64_t>(new_keys.size()));
-  if (rc) return rc;
-  for (size_t j = 0; j < pos.size(); ++j) h_slots[pos[j]] = got[j];
+  if (rc) {
+    kvx_slot_alloc_release(s->alloc, got.data(), static_cast<int64_t>(got.size()));
+    return rc;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    if (which[i] != SIZE_MAX) h_slots[i] = got[which[i]];
   return KVX_OK;
 }
 
@@ -161,9 +197,10 @@ int kvx_store_evict(kvx_store* s, const int64_t* h_keys, int64_t n) {
   std::vector<int64_t> v;
   int rc = lookup_host(s, h_keys, n, v);
   if (rc) return rc;
-  std::vector<int32_t> freed;
+  std::vector<int32_t> freed;  // each resident slot once, however often its key repeats
+  std::unordered_set<int64_t> seen;
   for (int64_t x : v)
-    if (x >= 0) freed.push_back(static_cast<int32_t>(x));
+    if (x >= 0 && seen.insert(x).second) freed.push_back(static_cast<int32_t>(x));
   kvx::DeviceGuard g(s->device);
   KVX_CUDA(cudaMemcpyAsync(s->d_scratch, h_keys, n * sizeof(int64_t), cudaMemcpyHostToDevice,
                            s->stream));
@@ -191,8 +228,9 @@ int kvx_store_migrate(kvx_store* src, kvx_store* dst, const int64_t* h_keys, int
   if (rc) return rc;
   std::vector<int64_t> keys;
   std::vector<int32_t> st;
+  std::unordered_set<int64_t> seen;
   for (int64_t i = 0; i < n; ++i)
-    if (d_have[i] < 0) {
+    if (d_have[i] < 0 && seen.insert(h_keys[i]).second) {
       keys.push_back(h_keys[i]);
       st.push_back(static_cast<int32_t>(s_slot[i]));
     }
@@ -204,28 +242,14 @@ int kvx_store_migrate(kvx_store* src, kvx_store* dst, const int64_t* h_keys, int
   // 3. bytes: src pool -> dst pool for every layer, K and V, on the source GPU
   // Across GPUs of one process the destination pool is reached through UVA
   // once peer access is on: the copy kernel's stores go over NVLink.
-  if (dst->device != src->device) {
-    rc = kvx_enable_peer(src->device, dst->device);
-    if (rc) return rc;
-  }
-  {
-    kvx::DeviceGuard g(src->device);
-    rc = ensure_scratch(src, m);
-    if (rc) return rc;
-    int32_t* d_tables = reinterpret_cast<int32_t*>(src->d_scratch);
-    KVX_CUDA(cudaMemcpyAsync(d_tables, st.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice,
-                             src->stream));
-    KVX_CUDA(cudaMemcpyAsync(d_tables + m, dt.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice,
-                             src->stream));
-    rc = kvx_copy_paged(src->pool, d_tables, dst->pool, d_tables + m, m, 0,
-                        kvx_pool_layers(src->pool), src->stream);
-    if (rc) return rc;
-    KVX_CUDA(cudaStreamSynchronize(src->stream));
-  }
+  rc = copy_blocks(src, dst, st, dt);
   // 4. land: index the new blocks at the destination
   std::vector<int64_t> vals(dt.begin(), dt.end());
-  rc = insert_host(dst, keys.data(), vals.data(), m);
-  if (rc) return rc;
+  if (!rc) rc = insert_host(dst, keys.data(), vals.data(), m);
+  if (rc) {  // nothing landed: give the destination slots back
+    kvx_slot_alloc_release(dst->alloc, dt.data(), m);
+    return rc;
+  }
   if (n_copied) *n_copied = m;
   return KVX_OK;
 }

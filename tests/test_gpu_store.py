@@ -77,3 +77,17 @@ def test_migrate_across_gpus(kvx):
                       stream=torch.cuda.current_stream(1))
         torch.cuda.synchronize(1)
     assert ctr.item() == 0
+
+
+def test_repeated_keys_take_one_slot(stores):
+    a, b = stores
+    slots = a.put([5, 6, 5, 7, 6, 5])
+    assert slots.tolist() == [0, 1, 0, 2, 1, 0]
+    a.evict([6, 6, 5])  # a key repeated in one evict frees its slot once
+    assert a.put([8, 9, 10]).tolist() == [0, 1, 3]
+    a_slots = a.put([11, 12])
+    assert b.put([]).tolist() == []
+    assert a.migrate_to(b, [11, 12, 11]) == 2  # duplicates land once
+    assert b.get([11, 12]).tolist() == [0, 1]
+    ctr = b.pool.verify(_t([0, 1]), 7, _t(a_slots), 0, 4)
+    assert ctr.item() == 0
