@@ -235,6 +235,12 @@ int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* ds
                    void* stream);
 /* Copy-kernel variant selector (0 = LSU 128-bit, 1 = TMA bulk); default 0. */
 int kvx_set_copy_impl(int impl);
+/* Block-table bounds: gather / scatter / paged copy skip any (layer, K|V,
+ * block) unit whose table entry is outside [0, slots) of its pool -- nothing
+ * is written outside a pool -- and flag it on the device.  Synchronizes
+ * `stream`, then returns KVX_EINVAL (and clears the flag) if an entry was out
+ * of range since the last check on this device, else KVX_OK. */
+int kvx_copy_check(void* stream);
 
 /* ---- stage 3: transfer engine ----------------------------------------- */
 

@@ -14,6 +14,7 @@ from .kvx import (  # noqa: F401
     ValidationError,
     chain_hash,
     chain_hash_batch,
+    copy_check,
     launch_count,
     match_prefix_batch,
     set_copy_impl,

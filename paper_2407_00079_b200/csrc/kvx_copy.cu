@@ -43,7 +43,13 @@ struct SlabCopy {
   int64_t n;       // blocks per plane
   int64_t planes;  // (hi - lo) * 2
   int64_t slab;    // bytes per unit, multiple of 16
+  uint32_t src_slots;  // valid table entries: [0, slots) (paged sides; < 2^31)
+  uint32_t dst_slots;
 };
+
+// Set when a table entry outside [0, slots) was met (that block is skipped,
+// not copied), per device; kvx_copy_check() reports and clears it.
+__device__ unsigned long long g_bad_table_entries = 0;
 
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
@@ -53,14 +59,21 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return r;
 }
 
-__device__ __forceinline__ void unit_addrs(const SlabCopy& c, int64_t u, const uint8_t*& s,
-                                           uint8_t*& d) {
+// Addresses of unit u; false (and flagged) when a table entry is out of range.
+__device__ __forceinline__ bool unit_addrs(const SlabCopy& c, int64_t u, const uint8_t*& s,
+                                           uint8_t*& d, bool count = false) {
   const int64_t plane = u / c.n;
   const int64_t b = u - plane * c.n;
-  const int64_t sb = c.src_table ? static_cast<int64_t>(__ldg(c.src_table + b)) : b;
-  const int64_t db = c.dst_table ? static_cast<int64_t>(__ldg(c.dst_table + b)) : b;
-  s = c.src + plane * c.src_plane + sb * c.slab;
-  d = c.dst + plane * c.dst_plane + db * c.slab;
+  // one unsigned 32-bit compare per side also rejects negative entries
+  const uint32_t sb = c.src_table ? static_cast<uint32_t>(__ldg(c.src_table + b))
+                                  : static_cast<uint32_t>(b);
+  const uint32_t db = c.dst_table ? static_cast<uint32_t>(__ldg(c.dst_table + b))
+                                  : static_cast<uint32_t>(b);
+  const bool ok = sb < c.src_slots && db < c.dst_slots;
+  s = c.src + plane * c.src_plane + static_cast<int64_t>(sb) * c.slab;
+  d = c.dst + plane * c.dst_plane + static_cast<int64_t>(db) * c.slab;
+  if (!ok && count) g_bad_table_entries = 1;  // a plain idempotent store: no atomics in the copy loop
+  return ok;
 }
 
 constexpr int kLsuThreads = 512;
@@ -77,8 +90,8 @@ __global__ void __launch_bounds__(kLsuThreads) copy_lsu_plain_kernel(const SlabC
     const int64_t off = (it - u * parts) * kLsuItem;
     const uint8_t* s;
     uint8_t* d;
-    unit_addrs(c, u, s, d);
-    const int64_t bytes = min(kLsuItem, c.slab - off);
+    const bool ok = unit_addrs(c, u, s, d, off == 0);
+    const int64_t bytes = ok ? min(kLsuItem, c.slab - off) : 0;
     const int4* sv = reinterpret_cast<const int4*>(s + off);
     int4* dv = reinterpret_cast<int4*>(d + off);
     const int nv = static_cast<int>(bytes >> 4);
@@ -119,8 +132,8 @@ __device__ __forceinline__ void lsu_copy(const SlabCopy& c) {
     const int64_t off = (it - u * parts) * kLsuItem;
     const uint8_t* s;
     uint8_t* d;
-    unit_addrs(c, u, s, d);
-    n = static_cast<int>(min(kLsuItem, c.slab - off) >> 4);
+    const bool ok = unit_addrs(c, u, s, d, off == 0);
+    n = ok ? static_cast<int>(min(kLsuItem, c.slab - off) >> 4) : 0;
     const int4* sv = reinterpret_cast<const int4*>(s + off);
     dst = reinterpret_cast<int4*>(d + off);
 #pragma unroll
@@ -232,14 +245,15 @@ __global__ void __launch_bounds__(32) copy_tma_kernel(const SlabCopy c) {
   // this CTA's items: blockIdx.x, blockIdx.x + gridDim.x, ...
   const int64_t mine = items > blockIdx.x ? (items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
-  auto item_addr = [&](int64_t k, const uint8_t*& s, uint8_t*& d, uint32_t& bytes) {
+  auto item_addr = [&](int64_t k, const uint8_t*& s, uint8_t*& d, uint32_t& bytes, bool count) {
     const int64_t it = blockIdx.x + k * gridDim.x;
     const int64_t u = it / parts;
     const int64_t off = (it - u * parts) * kStage;
-    unit_addrs(c, u, s, d);
+    const bool ok = unit_addrs(c, u, s, d);
     s += off;
     d += off;
-    bytes = static_cast<uint32_t>(min(kStage, c.slab - off));
+    bytes = ok ? static_cast<uint32_t>(min(kStage, c.slab - off)) : 0u;
+    if (!ok && count) g_bad_table_entries = 1;
   };
 
   for (int64_t k = 0; k < mine + AHEAD; ++k) {
@@ -251,8 +265,9 @@ __global__ void __launch_bounds__(32) copy_tma_kernel(const SlabCopy c) {
       const uint8_t* s;
       uint8_t* d;
       uint32_t bytes;
-      item_addr(kc, s, d, bytes);
-      bulk_store(d, smem + st * kStage, bytes);
+      item_addr(kc, s, d, bytes, false);
+      if (bytes) bulk_store(d, smem + st * kStage, bytes);
+      else asm volatile("cp.async.bulk.commit_group;" ::: "memory");  // keep the group count
     }
     // produce item k into its stage once the store that last used it (item
     // k - STAGES; stores committed so far: items <= kc) has read shared memory
@@ -262,9 +277,9 @@ __global__ void __launch_bounds__(32) copy_tma_kernel(const SlabCopy c) {
       const uint8_t* s;
       uint8_t* d;
       uint32_t bytes;
-      item_addr(k, s, d, bytes);
-      mbar_expect_tx(&bars[st], bytes);
-      bulk_load(smem + st * kStage, s, bytes, &bars[st]);
+      item_addr(k, s, d, bytes, true);
+      mbar_expect_tx(&bars[st], bytes);  // 0 bytes: the arrive alone completes the phase
+      if (bytes) bulk_load(smem + st * kStage, s, bytes, &bars[st]);
     }
   }
   bulk_wait_all();
@@ -363,6 +378,10 @@ __global__ void __launch_bounds__(256) verify_kernel(const uint8_t* __restrict__
     const int64_t b = u - plane * n;
     const int64_t layer = layer_lo + (plane >> 1);
     const int kv = static_cast<int>(plane & 1);
+    if (dst_table[b] < 0 || dst_table[b] >= slots || src_table[b] < 0) {  // out of range: all words bad
+      if (threadIdx.x == 0) bad += static_cast<unsigned long long>(words);
+      continue;
+    }
     const uint64_t seed = slab_seed(src_pool_id, static_cast<uint32_t>(layer),
                                     static_cast<uint32_t>(kv),
                                     static_cast<uint32_t>(src_table[b]));
@@ -518,6 +537,8 @@ int kvx_gather(const kvx_pool* p, const int32_t* d_src_table, int64_t n, int32_t
   c.dst_plane = n * p->slab;
   c.dst_table = nullptr;
   c.n = n;
+  c.src_slots = static_cast<uint32_t>(p->d.slots);
+  c.dst_slots = static_cast<uint32_t>(n);
   c.planes = static_cast<int64_t>(hi - lo) * 2;
   c.slab = p->slab;
   DeviceGuard g(p->d.device);
@@ -540,6 +561,8 @@ int kvx_scatter(kvx_pool* p, const int32_t* d_dst_table, int64_t n, int32_t lo, 
   c.dst_plane = p->d.slots * p->slab;
   c.dst_table = d_dst_table;
   c.n = n;
+  c.src_slots = static_cast<uint32_t>(n);
+  c.dst_slots = static_cast<uint32_t>(p->d.slots);
   c.planes = static_cast<int64_t>(hi - lo) * 2;
   c.slab = p->slab;
   DeviceGuard g(p->d.device);
@@ -563,10 +586,22 @@ int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* ds
   c.dst_plane = dst->d.slots * dst->slab;
   c.dst_table = d_dst_table;
   c.n = n;
+  c.src_slots = static_cast<uint32_t>(src->d.slots);
+  c.dst_slots = static_cast<uint32_t>(dst->d.slots);
   c.planes = static_cast<int64_t>(hi - lo) * 2;
   c.slab = src->slab;
   DeviceGuard g(src->d.device);
   return launch_copy(c, src->d.device, as_stream(stream));
+}
+
+int kvx_copy_check(void* stream) {
+  KVX_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  unsigned long long bad = 0, zero = 0;
+  KVX_CUDA(cudaMemcpyFromSymbol(&bad, g_bad_table_entries, sizeof(bad)));
+  if (bad == 0) return KVX_OK;
+  KVX_CUDA(cudaMemcpyToSymbol(g_bad_table_entries, &zero, sizeof(zero)));
+  return set_error(KVX_EINVAL,
+                   "block table entries out of [0, slots): those blocks were skipped, not copied");
 }
 
 }  // extern "C"

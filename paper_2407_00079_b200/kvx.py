@@ -116,6 +116,7 @@ _sig("kvx_gather", C.c_int, _vp, _vp, _i64, _i32, _i32, _vp, _vp)
 _sig("kvx_scatter", C.c_int, _vp, _vp, _i64, _i32, _i32, _vp, _vp)
 _sig("kvx_copy_paged", C.c_int, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp)
 _sig("kvx_set_copy_impl", C.c_int, C.c_int)
+_sig("kvx_copy_check", C.c_int, _vp)
 _sig("kvx_xfer_create", C.c_int, C.c_int, C.POINTER(_vp))
 _sig("kvx_xfer_destroy", C.c_int, _vp)
 _sig("kvx_xfer_stream", _vp, _vp)
@@ -192,6 +193,13 @@ def _ptr(t: Optional[torch.Tensor]):
 def set_copy_impl(impl: str) -> None:
     """'lsu' (128-bit loads/stores) or 'tma' (cp.async.bulk pipeline)."""
     check(_L.kvx_set_copy_impl({"lsu": 0, "tma": 1}[impl]))
+
+
+def copy_check(stream=None) -> None:
+    """Raise ValidationError (KVX_EINVAL) if a gather / scatter / paged copy met a block
+    table entry outside [0, slots) since the last check on the current device
+    (that block was skipped, not copied).  Synchronizes `stream`."""
+    check(_L.kvx_copy_check(_stream(stream)))
 
 
 # ---- stage 1a ---------------------------------------------------------------

@@ -88,6 +88,31 @@ def test_empty_and_bad_ranges(kvx):
         kvx.KVPool(2, 16, 8, 128, 3, 4, 0)
 
 
+@pytest.mark.parametrize("impl", IMPLS)
+def test_out_of_range_table_entries_are_skipped(kvx, impl):
+    """Entries outside [0, slots) (incl. negative) never write outside a pool:
+    those units are skipped, the rest copied, and kvx_copy_check reports it."""
+    kvx.set_copy_impl(impl)
+    src = kvx.KVPool(2, 16, 8, 128, 2, 6, 0)
+    dst = kvx.KVPool(2, 16, 8, 128, 2, 6, 0)
+    src.fill_synthetic(5)
+    guard = dst.tensor_view()
+    guard.fill_(0xAB)
+    kvx.copy_check()  # clean slate
+    src.copy_to(dst, _t([0, 9, 2, -1]), _t([1, 2, 6, 3]), 0, 2)
+    with pytest.raises(kvx.ValidationError):
+        kvx.copy_check()
+    kvx.copy_check()  # the flag was cleared
+    ctr = dst.verify(_t([1]), 5, _t([0]), 0, 2)  # the valid unit landed
+    assert ctr.item() == 0
+    host = _host(dst).reshape(2, 2, 6, -1)
+    assert (host[:, :, [0, 2, 3, 4, 5]] == 0xAB).all()  # skipped units wrote nothing
+    buf = torch.zeros(3 * 2 * 2 * src.slab, dtype=torch.uint8, device=DEV)
+    src.gather(_t([0, 6, 1]), 0, 2, buf.data_ptr())
+    with pytest.raises(kvx.ValidationError):
+        kvx.copy_check()
+
+
 def test_transfer_engine_local(kvx):
     eng = kvx.TransferEngine(0)
     a = torch.arange(1 << 20, dtype=torch.int64, device=DEV)
