@@ -60,18 +60,20 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
 }
 
 // Addresses of unit u; false (and flagged) when a table entry is out of range.
-__device__ __forceinline__ bool unit_addrs(const SlabCopy& c, int64_t u, const uint8_t*& s,
+template <class Idx = int64_t>
+__device__ __forceinline__ bool unit_addrs(const SlabCopy& c, Idx u, const uint8_t*& s,
                                            uint8_t*& d, bool count = false) {
-  const int64_t plane = u / c.n;
-  const int64_t b = u - plane * c.n;
+  const Idx n = static_cast<Idx>(c.n);
+  const Idx plane = u / n;
+  const Idx b = u - plane * n;
   // one unsigned 32-bit compare per side also rejects negative entries
   const uint32_t sb = c.src_table ? static_cast<uint32_t>(__ldg(c.src_table + b))
                                   : static_cast<uint32_t>(b);
   const uint32_t db = c.dst_table ? static_cast<uint32_t>(__ldg(c.dst_table + b))
                                   : static_cast<uint32_t>(b);
   const bool ok = sb < c.src_slots && db < c.dst_slots;
-  s = c.src + plane * c.src_plane + static_cast<int64_t>(sb) * c.slab;
-  d = c.dst + plane * c.dst_plane + static_cast<int64_t>(db) * c.slab;
+  s = c.src + static_cast<int64_t>(plane) * c.src_plane + static_cast<int64_t>(sb) * c.slab;
+  d = c.dst + static_cast<int64_t>(plane) * c.dst_plane + static_cast<int64_t>(db) * c.slab;
   if (!ok && count) g_bad_table_entries = 1;  // a plain idempotent store: no atomics in the copy loop
   return ok;
 }
@@ -120,19 +122,22 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
 // loads issued before the current item's stores (8 x 16 B in flight per
 // thread).  r01: 0.966 of the measured HBM copy peak vs 0.951 for the plain
 // form.
-template <bool kCsStores, bool kPipelined>
+// Idx: uint32_t when the launch has < 2^32 work items (the host checks), so
+// the per-item index arithmetic is 32-bit (64-bit division is a long
+// subroutine that also cost the kernel register spills).
+template <bool kCsStores, bool kPipelined, class Idx>
 __device__ __forceinline__ void lsu_copy(const SlabCopy& c) {
-  const int64_t parts = (c.slab + kLsuItem - 1) / kLsuItem;
-  const int64_t items = c.planes * c.n * parts;
+  const Idx parts = static_cast<Idx>((c.slab + kLsuItem - 1) / kLsuItem);
+  const Idx items = static_cast<Idx>(c.planes * c.n * parts);
   int4 r[kLsuUnroll];
   int nv = 0;
   int4* dv = nullptr;
-  auto load = [&](int64_t it, int4 (&buf)[kLsuUnroll], int& n, int4*& dst) {
-    const int64_t u = it / parts;
-    const int64_t off = (it - u * parts) * kLsuItem;
+  auto load = [&](Idx it, int4 (&buf)[kLsuUnroll], int& n, int4*& dst) {
+    const Idx u = it / parts;
+    const int64_t off = static_cast<int64_t>(it - u * parts) * kLsuItem;
     const uint8_t* s;
     uint8_t* d;
-    const bool ok = unit_addrs(c, u, s, d, off == 0);
+    const bool ok = unit_addrs<Idx>(c, u, s, d, off == 0);
     n = ok ? static_cast<int>(min(kLsuItem, c.slab - off) >> 4) : 0;
     const int4* sv = reinterpret_cast<const int4*>(s + off);
     dst = reinterpret_cast<int4*>(d + off);
@@ -152,7 +157,7 @@ __device__ __forceinline__ void lsu_copy(const SlabCopy& c) {
       }
     }
   };
-  int64_t it = blockIdx.x;
+  Idx it = blockIdx.x;
   if (it >= items) return;
   load(it, r, nv, dv);
   for (; it < items; it += gridDim.x) {
@@ -173,8 +178,9 @@ __device__ __forceinline__ void lsu_copy(const SlabCopy& c) {
   }
 }
 
+template <class Idx>
 __global__ void __launch_bounds__(kLsuThreads, 2) copy_lsu_kernel(const SlabCopy c) {
-  lsu_copy<true, true>(c);
+  lsu_copy<true, true, Idx>(c);
 }
 
 // ---- TMA bulk-copy pipeline ----------------------------------------------
@@ -338,7 +344,8 @@ int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
       return e ? std::atoi(e) : 0;
     }();
     if (variant == 1) copy_lsu_plain_kernel<<<blocks, kLsuThreads, 0, s>>>(c);
-    else copy_lsu_kernel<<<blocks, kLsuThreads, 0, s>>>(c);
+    else if (items + blocks < (int64_t{1} << 32)) copy_lsu_kernel<uint32_t><<<blocks, kLsuThreads, 0, s>>>(c);
+    else copy_lsu_kernel<int64_t><<<blocks, kLsuThreads, 0, s>>>(c);
     KVX_LAUNCH_CHECK("copy_lsu_kernel");
   }
   return KVX_OK;
