@@ -11,6 +11,7 @@ import collections
 import csv
 import io
 import json
+import re
 import os
 import subprocess
 import sys
@@ -54,8 +55,9 @@ def raw(rep):
     h, units = rows[0], rows[1]
     out = []
     for vals in rows[2:]:
-        d = {"kernel": vals[h.index("Kernel Name")].split("(")[0].replace("kvx::<unnamed>::", "")
-             .replace("unnamed>::", "")}
+        name = vals[h.index("Kernel Name")].split("(")[0].replace("kvx::<unnamed>::", "") \
+            .replace("unnamed>::", "")
+        d = {"kernel": re.sub(r"^void |<.*>$", "", name)}  # copy_lsu_kernel<unsigned int> -> copy_lsu_kernel
         for m in METRICS:
             if m in h:
                 i = h.index(m)
