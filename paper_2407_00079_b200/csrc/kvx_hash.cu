@@ -224,9 +224,15 @@ __global__ void __launch_bounds__(kHashThreads, KVX_HASH_MIN_CTAS) block_hash_fu
     t0 = __shfl_sync(0xffffffffu, t0, 0);
     if (t0 >= tasks) break;
     const int64_t t_end = min(t0 + kClaim, tasks);
+    // window-major: task t = (window w = t / n_req, request r = t % n_req), every
+    // request's window w before any w+1; one division per claim, then step
+    int64_t w = t0 / n_req;
+    int64_t r = t0 - w * n_req - 1;
     for (int64_t t = t0; t < t_end; ++t) {
-      const int64_t w = t / n_req;  // window-major: every request's window w before any w+1
-      const int64_t r = t - w * n_req;
+      if (++r == n_req) {
+        r = 0;
+        ++w;
+      }
       const int64_t k0 = key_off[r];
       const int64_t nblk = key_off[r + 1] - k0;
       if (w * 32 >= nblk) continue;  // warp-uniform: request shorter than this window
