@@ -241,7 +241,10 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
        t < tasks; t += warps) {
-    const int64_t r = t / p.n_inst;
+    // 32-bit division when it suffices (a 64-bit one is a long subroutine)
+    const int64_t r = tasks <= 0xFFFFFFFFll
+                          ? static_cast<int64_t>(static_cast<uint32_t>(t) / static_cast<uint32_t>(p.n_inst))
+                          : t / p.n_inst;
     const int i = static_cast<int>(t - r * p.n_inst);
     const int64_t* __restrict__ tk = p.keys[i];
     const uint64_t mask = p.mask[i];
