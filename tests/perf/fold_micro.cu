@@ -139,6 +139,30 @@ __global__ void fold_vec(const int64_t* key_off, int64_t* keys, int n_req) {
   }
 }
 
+// Bandwidth hog for the "under load" variants: streams a large buffer on the
+// other SMs (like the content producers streaming token ids).
+__global__ void hog(const int4* __restrict__ a, int4* __restrict__ b, int64_t n, int reps) {
+  for (int r = 0; r < reps; ++r)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      b[i] = a[i];
+}
+
+// Same hog with L2 evict-first loads and streaming stores (does not displace the fold's keys).
+__global__ void hog_ef(const int4* __restrict__ a, int4* __restrict__ b, int64_t n, int reps) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  for (int r = 0; r < reps; ++r)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      int4 q;
+      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                   : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(a + i), "l"(pol));
+      asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(b + i), "r"(q.x),
+                   "r"(q.y), "r"(q.z), "r"(q.w), "l"(pol) : "memory");
+    }
+}
+
 int main() {
   std::vector<int64_t> off(kReq + 1);
   for (int i = 0; i <= kReq; ++i) off[i] = static_cast<int64_t>(i) * kBlk;
@@ -151,7 +175,14 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   float ms;
-  for (int v = 0; v < 10; ++v) {
+  // hog: 2 x 1 GiB buffers, run on 116 SMs' worth of CTAs on a second stream
+  const int64_t hn = (1LL << 30) / 16;
+  int4 *ha, *hb;
+  cudaMalloc(&ha, hn * 16);
+  cudaMalloc(&hb, hn * 16);
+  cudaStream_t hs;
+  cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking);
+  for (int v = 0; v < 16; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       if (v == 0) fold_strided<<<kReq / 32, 32>>>(d_off, d_keys, kReq, 1);
@@ -164,6 +195,26 @@ int main() {
       if (v == 7) fold_vec<8><<<kReq / 128, 128>>>(d_off, d_keys, kReq);
       if (v == 8) fold_vec<16><<<kReq / 32, 32>>>(d_off, d_keys, kReq);
       if (v == 9) fold_vec<16><<<kReq / 128, 128>>>(d_off, d_keys, kReq);
+      if (v >= 10) {
+        // fold first (it takes the first 32 SMs), then the hog fills the rest
+        cudaStream_t fs;
+        cudaStreamCreateWithFlags(&fs, cudaStreamNonBlocking);
+        cudaEventRecord(a, fs);
+        // 200 KB of (unused) shared memory keeps the hog's CTAs off the folding SMs
+        const int excl = 200 * 1024;
+        cudaFuncSetAttribute(fold_vec<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, excl);
+        cudaFuncSetAttribute(fold_strided, cudaFuncAttributeMaxDynamicSharedMemorySize, excl);
+        if (v == 10 || v == 12 || v == 14) fold_vec<8><<<kReq / 128, 128, excl, fs>>>(d_off, d_keys, kReq);
+        else fold_strided<<<kReq / 128, 128, excl, fs>>>(d_off, d_keys, kReq, 1);
+        // v 10/11: hog saturates HBM; v 12/13: a light hog (~16 CTAs)
+        if (v < 14) hog<<<v < 12 ? 116 * 4 : 16, 512, 0, hs>>>(ha, hb, hn, v < 12 ? 4 : 1);
+        else hog_ef<<<16, 512, 0, hs>>>(ha, hb, hn, 1);
+        cudaEventRecord(b, fs);
+        cudaEventSynchronize(b);
+        cudaStreamSynchronize(hs);
+        cudaStreamDestroy(fs);
+        continue;
+      }
       cudaEventRecord(b);
       cudaEventSynchronize(b);
     }
@@ -171,7 +222,9 @@ int main() {
     const char* names[] = {"strided load+store", "strided load only", "smem transposed",
                            "registers only", "2 requests/lane", "a) 4 warps/CTA",
                            "f) vec8 1 warp/CTA", "f) vec8 4 warps/CTA", "f) vec16 1 warp/CTA",
-                           "f) vec16 4 warps/CTA"};
+                           "f) vec16 4 warps/CTA", "f) vec8 4w + HBM hog", "a) 4w + HBM hog",
+                           "f) vec8 4w + light hog", "a) 4w + light hog",
+                           "f) vec8 4w + light evict-first hog", "a) 4w + light evict-first hog"};
     std::printf("%-20s %8.1f us  = %.1f cycles/step @1.965GHz\n", names[v], ms * 1e3,
                 ms * 1e-3 * 1.965e9 / kBlk);
   }
