@@ -64,6 +64,9 @@ def parse_args():
     ap.add_argument("--block-size", type=int, default=16)
     ap.add_argument("--dtype-bytes", type=int, default=2)
     ap.add_argument("--no-match", action="store_true")
+    ap.add_argument("--match-exchange", default="nvlink", choices=["nvlink", "nccl"],
+                    help="N>1 prefix match: combine the per-GPU instances inside the match "
+                         "kernel (NVLink remote atomics + stream flags) or by NCCL all-reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -640,6 +643,15 @@ def bench_match(args, dev, rank, world, role):
         best_id = torch.empty(mw.n_req, dtype=torch.int32, device=d)
         packed = torch.empty(mw.n_req, dtype=torch.int64, device=d)
     s.synchronize()
+    xm = None
+    if world > 1 and args.match_exchange == "nvlink":
+        # the exchange inside the match kernel: remote atomicMax into every
+        # rank's result buffer over NVLink + stream-ordered flags (kvx_xmatch)
+        xm = pkg.kvx.XMatch(dev, rank, world, mw.n_req)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, xm.export())
+        for blob in blobs:
+            xm.connect(blob)
     st = idx.stats()
     assert st["live"] == mw.pool_keys, st
     mw.index_keys = index_keys.cpu().numpy()
@@ -656,10 +668,13 @@ def bench_match(args, dev, rank, world, role):
         if world == 1:
             pkg.match_prefix_batch([idx], [0], keys, key_off, want_lens=False, stream=s,
                                    out=(None, best_len, best_id))
-        else:  # local best per request, then the cross-GPU exchange: all-reduce(MAX)
+            tm.stop(s, b, 0)
+        elif xm is not None:  # match + cross-GPU MAX in one kernel (NVLink atomics), flags
+            xm.run([idx], [rank], keys, key_off, out=(best_len, best_id), stream=s)
+            tm.stop(s, b, 0)
+        else:  # local best per request, then the cross-GPU exchange: NCCL all-reduce(MAX)
             pkg.kvx.match_prefix_packed([idx], [rank], keys, key_off, out=packed, stream=s)
-        tm.stop(s, b, 0)
-        if world > 1:
+            tm.stop(s, b, 0)
             with torch.cuda.stream(s):
                 dist.all_reduce(packed, op=dist.ReduceOp.MAX)
             best_len, best_id = pkg.kvx.best_unpack(packed, stream=s)
@@ -798,7 +813,11 @@ def bench_match(args, dev, rank, world, role):
         "config": {**mw.describe(), "instances": world,
                    "layout": ("one instance index" if world == 1 else
                               "one prefill instance index per GPU; per-request best combined "
-                              "by all-reduce(MAX) over packed (len<<32 | ~id) words (NCCL)")},
+                              + ("inside the match kernel: atomicMax of packed (len<<32 | ~id) "
+                                 "words into every GPU's result buffer over NVLink, stream-"
+                                 "ordered flags (kvx_xmatch, no collective)"
+                                 if args.match_exchange == "nvlink" else
+                                 "by all-reduce(MAX) over packed (len<<32 | ~id) words (NCCL)"))},
         "kernels": {
             "block_hash_kernel": {
                 "avg_ms": hs["avg_ms"], "bytes": hs["avg_algorithmic_bytes"],

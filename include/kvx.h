@@ -132,6 +132,25 @@ int kvx_match_prefix_packed(const kvx_index* const* idx, const int32_t* inst_ids
 int kvx_best_unpack(const uint64_t* d_packed, int64_t n_req, int64_t* d_best_len,
                     int32_t* d_best_id, void* stream);
 
+/* Cross-GPU find_best_prefix_match WITHOUT a collective (SURVEY 8(e) case
+ * ii; replaces kvx_match_prefix_packed + all-reduce(MAX) + kvx_best_unpack):
+ * `world` processes, one per GPU, each holding some prefill instances.  Every
+ * rank's match kernel atomically MAXes each request's packed word straight
+ * into every rank's result buffer over NVLink (CUDA IPC mappings); stream-
+ * ordered 64-bit flags then tell each rank that all ranks' atomics landed.
+ * Setup: create on every rank, exchange the export blobs (any side channel),
+ * connect each rank to every other.  kvx_xmatch_run is collective: every
+ * rank calls it once per batch, same n_req, in the same order. */
+#define KVX_MAX_PEERS 8
+typedef struct kvx_xmatch kvx_xmatch;
+int kvx_xmatch_create(int device, int rank, int world, int64_t max_req, kvx_xmatch** out);
+int kvx_xmatch_destroy(kvx_xmatch* x);
+int kvx_xmatch_export(kvx_xmatch* x, uint8_t* blob, int64_t cap, int64_t* len);
+int kvx_xmatch_connect(kvx_xmatch* x, const uint8_t* blob, int64_t len);
+int kvx_xmatch_run(kvx_xmatch* x, const kvx_index* const* idx, const int32_t* inst_ids,
+                   int64_t n_inst, const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+                   int64_t* d_best_len, int32_t* d_best_id, void* stream);
+
 /* ---- batched Conductor scoring (kvcache-centric schedule, FP64) -------- */
 
 /* Mirrors of kvcsim::PerfModelParams (proj/include/kvcsim/perf_model.hpp:13-26),

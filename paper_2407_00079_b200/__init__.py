@@ -12,6 +12,7 @@ from .kvx import (  # noqa: F401
     KvxError,
     TransferEngine,
     ValidationError,
+    XMatch,
     chain_hash,
     chain_hash_batch,
     copy_check,

@@ -21,6 +21,7 @@
 // per-request argmax over instances is one atomicMax per task on a packed
 // (len << 32 | ~id) word, which reproduces the lowest-id tie-break.
 #include <algorithm>
+#include <cstring>
 
 #include "kvx_common.cuh"
 
@@ -181,6 +182,10 @@ struct MatchParams {
   int32_t ids[KVX_MAX_INSTANCES];
   int32_t n_inst;
   int32_t packed_only;  // leave the packed (len<<32 | ~id) word for a cross-GPU MAX
+  // cross-GPU exchange inside the kernel: atomicMax of the packed word into
+  // every rank's result buffer (peer mappings; NVLink remote atomics)
+  unsigned long long* dests[KVX_MAX_PEERS];
+  int32_t n_dests;
 };
 
 // U independent probe chains per lane: every chain's next slot load is issued
@@ -275,7 +280,10 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
     }
     if (lane == 0) {
       if (len_out) len_out[t] = len;
-      if (best_len) {
+      if (p.n_dests > 0) {
+        const unsigned long long v = pack_best(len, p.ids[i]);
+        for (int j = 0; j < p.n_dests; ++j) atomicMax(p.dests[j] + r, v);
+      } else if (best_len) {
         if (p.n_inst == 1 && !p.packed_only) {
           best_len[r] = len;
           best_id[r] = p.ids[0];
@@ -384,7 +392,7 @@ int ensure_room(kvx_index* x, int64_t n, cudaStream_t s) {
 int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
                const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
                int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id, bool packed_only,
-               void* stream);
+               void* stream, uint64_t* const* dests = nullptr, int n_dests = 0);
 
 }  // namespace
 
@@ -569,10 +577,12 @@ namespace {
 int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
                const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
                int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id, bool packed_only,
-               void* stream) {
+               void* stream, uint64_t* const* dests, int n_dests) {
   MatchParams p{};
   p.n_inst = static_cast<int32_t>(n_inst);
   p.packed_only = packed_only ? 1 : 0;
+  p.n_dests = n_dests;
+  for (int j = 0; j < n_dests; ++j) p.dests[j] = reinterpret_cast<unsigned long long*>(dests[j]);
   const int dev = idx[0] ? idx[0]->device : -1;
   for (int64_t i = 0; i < n_inst; ++i) {
     KVX_REQUIRE(idx[i] != nullptr, "kvx_match_prefix_batch: NULL index");
@@ -583,7 +593,7 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
   }
   DeviceGuard g(dev);
   cudaStream_t s = as_stream(stream);
-  if (d_best_len && (n_inst > 1 || packed_only))
+  if (d_best_len && (n_inst > 1 || packed_only) && n_dests == 0)
     KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
   const int threads = 256;
   const int64_t tasks = n_req * n_inst;
@@ -601,3 +611,152 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
   return KVX_OK;
 }
 }  // namespace
+
+// ---- cross-GPU best match without a collective --------------------------
+// SURVEY 8(e) case ii: one prefill instance (or several) per GPU.  The match
+// kernel of every rank atomically MAXes each request's packed word straight
+// into EVERY rank's result buffer through CUDA IPC mappings (NVLink remote
+// atomics), so the exchange is part of the kernel; 64-bit flags written with
+// stream memory operations then tell each rank that all ranks' atomics have
+// landed (no kernel spins on another's flag).  Result buffers are double
+// buffered by step parity: a rank zeroes the buffer for step e+1 before it
+// announces step e, and every rank starts step e+1 only after all step-e
+// announcements, so no atomic can hit a buffer before it was zeroed.
+struct kvx_xmatch {
+  int device = 0, rank = 0, world = 1;
+  int64_t max_req = 0;
+  uint8_t* mem = nullptr;  // [buf0 | buf1 | flags[KVX_MAX_PEERS]]
+  uint64_t* peer_buf[KVX_MAX_PEERS][2] = {};
+  uint64_t* peer_flags[KVX_MAX_PEERS] = {};
+  void* peer_mem[KVX_MAX_PEERS] = {};
+  uint64_t epoch = 0;
+  uint64_t* buf(int b) const { return reinterpret_cast<uint64_t*>(mem) + b * max_req; }
+  uint64_t* flags() const { return reinterpret_cast<uint64_t*>(mem) + 2 * max_req; }
+  size_t bytes() const { return (2 * static_cast<size_t>(max_req) + KVX_MAX_PEERS) * sizeof(uint64_t); }
+};
+
+namespace {
+struct XmatchBlob {
+  int32_t magic, rank, world, pad;
+  int64_t max_req;
+  uint8_t handle[KVX_IPC_HANDLE_BYTES];
+};
+constexpr int32_t kXmatchMagic = 0x6b76786d;  // "kvxm"
+}  // namespace
+
+extern "C" {
+
+int kvx_xmatch_create(int device, int rank, int world, int64_t max_req, kvx_xmatch** out) {
+  KVX_REQUIRE(out != nullptr, "kvx_xmatch_create: NULL out");
+  KVX_REQUIRE(world >= 1 && world <= KVX_MAX_PEERS && rank >= 0 && rank < world,
+              "kvx_xmatch_create: bad rank / world");
+  KVX_REQUIRE(max_req >= 1, "kvx_xmatch_create: max_req must be >= 1");
+  DeviceGuard g(device);
+  auto* x = new kvx_xmatch();
+  x->device = device;
+  x->rank = rank;
+  x->world = world;
+  x->max_req = max_req;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&x->mem), x->bytes());
+  if (e == cudaSuccess) e = cudaMemset(x->mem, 0, x->bytes());
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any peer maps it
+  if (e != cudaSuccess) {
+    kvx_xmatch_destroy(x);
+    return cuda_error(e, "kvx_xmatch_create");
+  }
+  x->peer_buf[rank][0] = x->buf(0);
+  x->peer_buf[rank][1] = x->buf(1);
+  x->peer_flags[rank] = x->flags();
+  *out = x;
+  return KVX_OK;
+}
+
+int kvx_xmatch_destroy(kvx_xmatch* x) {
+  if (!x) return KVX_OK;
+  DeviceGuard g(x->device);
+  cudaDeviceSynchronize();
+  for (int j = 0; j < KVX_MAX_PEERS; ++j)
+    if (x->peer_mem[j]) kvx_ipc_close(x->peer_mem[j]);
+  if (x->mem) cudaFree(x->mem);
+  delete x;
+  return KVX_OK;
+}
+
+int kvx_xmatch_export(kvx_xmatch* x, uint8_t* blob, int64_t cap, int64_t* len) {
+  KVX_REQUIRE(x && len, "kvx_xmatch_export: NULL argument");
+  *len = static_cast<int64_t>(sizeof(XmatchBlob));
+  if (!blob) return KVX_OK;
+  KVX_REQUIRE(cap >= *len, "kvx_xmatch_export: blob too small");
+  XmatchBlob b{};
+  b.magic = kXmatchMagic;
+  b.rank = x->rank;
+  b.world = x->world;
+  b.max_req = x->max_req;
+  int rc = kvx_ipc_export(x->mem, b.handle);
+  if (rc) return rc;
+  std::memcpy(blob, &b, sizeof(b));
+  return KVX_OK;
+}
+
+int kvx_xmatch_connect(kvx_xmatch* x, const uint8_t* blob, int64_t len) {
+  KVX_REQUIRE(x && blob && len >= static_cast<int64_t>(sizeof(XmatchBlob)),
+              "kvx_xmatch_connect: bad blob");
+  XmatchBlob b;
+  std::memcpy(&b, blob, sizeof(b));
+  KVX_REQUIRE(b.magic == kXmatchMagic && b.world == x->world && b.max_req == x->max_req &&
+                  b.rank >= 0 && b.rank < x->world,
+              "kvx_xmatch_connect: peer does not match");
+  if (b.rank == x->rank) return KVX_OK;  // self
+  KVX_REQUIRE(x->peer_mem[b.rank] == nullptr, "kvx_xmatch_connect: peer already connected");
+  void* p = nullptr;
+  int rc = kvx_ipc_open(b.handle, x->device, &p);
+  if (rc) return rc;
+  x->peer_mem[b.rank] = p;
+  auto* words = static_cast<uint64_t*>(p);
+  x->peer_buf[b.rank][0] = words;
+  x->peer_buf[b.rank][1] = words + x->max_req;
+  x->peer_flags[b.rank] = words + 2 * x->max_req;
+  return KVX_OK;
+}
+
+int kvx_xmatch_run(kvx_xmatch* x, const kvx_index* const* idx, const int32_t* inst_ids,
+                   int64_t n_inst, const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+                   int64_t* d_best_len, int32_t* d_best_id, void* stream) {
+  KVX_REQUIRE(x != nullptr, "kvx_xmatch_run: NULL exchange");
+  KVX_REQUIRE(n_inst >= 1, "find_best_prefix_match: empty prefill pool");
+  KVX_REQUIRE(n_inst <= KVX_MAX_INSTANCES, "kvx_xmatch_run: too many instances");
+  KVX_REQUIRE(idx != nullptr && inst_ids != nullptr, "kvx_xmatch_run: NULL instances");
+  KVX_REQUIRE(n_req >= 0 && n_req <= x->max_req, "kvx_xmatch_run: n_req out of range");
+  KVX_REQUIRE(d_keys && d_key_off && d_best_len && d_best_id, "kvx_xmatch_run: NULL array");
+  for (int j = 0; j < x->world; ++j)
+    KVX_REQUIRE(x->peer_buf[j][0] != nullptr, "kvx_xmatch_run: not connected to every rank");
+  DeviceGuard g(x->device);
+  cudaStream_t s = as_stream(stream);
+  const uint64_t e = ++x->epoch;
+  const int b = static_cast<int>(e & 1);
+  uint64_t* dests[KVX_MAX_PEERS];
+  for (int j = 0; j < x->world; ++j) dests[j] = x->peer_buf[j][b];
+  if (n_req > 0) {
+    int rc = match_impl(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, nullptr, nullptr, nullptr,
+                        true, stream, dests, x->world);
+    if (rc) return rc;
+  }
+  // the other parity's buffer was unpacked last step: zero it before announcing
+  KVX_CUDA(cudaMemsetAsync(x->buf(b ^ 1), 0, sizeof(uint64_t) * x->max_req, s));
+  for (int j = 0; j < x->world; ++j) {  // "my atomics for step e have landed" -> every rank
+    int rc = kvx_signal_write(stream, x->peer_flags[j] + x->rank, e);
+    if (rc) return rc;
+  }
+  for (int j = 0; j < x->world; ++j) {  // wait for every rank's announcement
+    int rc = kvx_signal_wait(stream, x->flags() + j, e);
+    if (rc) return rc;
+  }
+  if (n_req > 0) {
+    unpack_best_kernel<<<grid_for(n_req, 256, x->device), 256, 0, s>>>(
+        reinterpret_cast<const unsigned long long*>(x->buf(b)), d_best_len, d_best_id, n_req);
+    KVX_LAUNCH_CHECK("unpack_best_kernel");
+  }
+  return KVX_OK;
+}
+
+}  // extern "C"

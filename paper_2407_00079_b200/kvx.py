@@ -104,6 +104,12 @@ _sig("kvx_match_prefix_batch", C.c_int, C.POINTER(_vp), C.POINTER(_i32), _i64, _
 _sig("kvx_match_prefix_packed", C.c_int, C.POINTER(_vp), C.POINTER(_i32), _i64, _vp, _vp, _i64,
      _vp, _vp)
 _sig("kvx_best_unpack", C.c_int, _vp, _i64, _vp, _vp, _vp)
+_sig("kvx_xmatch_create", C.c_int, C.c_int, C.c_int, C.c_int, _i64, C.POINTER(_vp))
+_sig("kvx_xmatch_destroy", C.c_int, _vp)
+_sig("kvx_xmatch_export", C.c_int, _vp, C.c_char_p, _i64, C.POINTER(_i64))
+_sig("kvx_xmatch_connect", C.c_int, _vp, C.c_char_p, _i64)
+_sig("kvx_xmatch_run", C.c_int, _vp, C.POINTER(_vp), C.POINTER(_i32), _i64, _vp, _vp, _i64, _vp,
+     _vp, _vp)
 _sig("kvx_pool_create", C.c_int, C.POINTER(KvxPoolDesc), C.POINTER(_vp))
 _sig("kvx_pool_create_view", C.c_int, C.POINTER(KvxPoolDesc), _vp, C.POINTER(_vp))
 _sig("kvx_pool_destroy", C.c_int, _vp)
@@ -319,6 +325,49 @@ def match_prefix_packed(indices: Sequence[BlockIndex], inst_ids: Sequence[int],
     check(_L.kvx_match_prefix_packed(arr, ids, n_inst, _ptr(keys) if keys.numel() else None,
                                      _ptr(key_off), n_req, _ptr(out), _stream(stream)))
     return out
+
+
+class XMatch:
+    """Cross-GPU find_best_prefix_match without a collective (kvx_xmatch_*):
+    every rank's match kernel MAXes its packed words into every rank's result
+    buffer over NVLink, stream-ordered flags close the step.  Create on every
+    rank, exchange ``export()`` blobs, ``connect`` every blob (own included is
+    a no-op), then call ``run`` on every rank once per batch."""
+
+    def __init__(self, device: int, rank: int, world: int, max_req: int):
+        h = _vp()
+        check(_L.kvx_xmatch_create(device, rank, world, max_req, C.byref(h)))
+        self.h, self.device, self.rank, self.world = h, device, rank, world
+
+    def export(self) -> bytes:
+        n = _i64()
+        check(_L.kvx_xmatch_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        check(_L.kvx_xmatch_export(self.h, buf, n.value, C.byref(n)))
+        return buf.raw[: n.value]
+
+    def connect(self, blob: bytes) -> None:
+        check(_L.kvx_xmatch_connect(self.h, blob, len(blob)))
+
+    def run(self, indices: Sequence[BlockIndex], inst_ids: Sequence[int], keys: torch.Tensor,
+            key_off: torch.Tensor, out=None, stream=None):
+        n_inst = len(indices)
+        n_req = len(key_off) - 1
+        arr = (_vp * max(n_inst, 1))(*[i.h for i in indices])
+        ids = (_i32 * max(n_inst, 1))(*[int(i) for i in inst_ids])
+        if out is None:
+            out = (torch.empty(n_req, dtype=torch.int64, device=keys.device),
+                   torch.empty(n_req, dtype=torch.int32, device=keys.device))
+        best_len, best_id = out
+        check(_L.kvx_xmatch_run(self.h, arr, ids, n_inst, _ptr(keys) if keys.numel() else None,
+                                _ptr(key_off), n_req, _ptr(best_len), _ptr(best_id),
+                                _stream(stream)))
+        return best_len, best_id
+
+    def __del__(self):
+        if getattr(self, "h", None) and alive():
+            _L.kvx_xmatch_destroy(self.h)
+            self.h = None
 
 
 def best_unpack(packed: torch.Tensor, stream=None):
