@@ -461,7 +461,8 @@ __global__ void __launch_bounds__(1024) order_kernel(const int64_t* __restrict__
 
 // V independent request streams per half-warp (every lane advances V chains
 // per step).  V = 1 is the shipped kernel: V = 2 was slower on the Config 4
-// batch (254 vs 198 us at equal chains per SM, profiles/r01/hash_halfwarp.md).
+// batch at every width, also with a compact (select-only, unroll 4) step loop
+// (profiles/r01/hash_halfwarp.md).
 template <int V>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
