@@ -226,7 +226,10 @@ __device__ __forceinline__ void probe_multi(const int64_t* __restrict__ tk, uint
   }
 }
 
-constexpr int kProbeChains = 4;  // per lane -> 128 query keys per warp step
+#ifndef KVX_PROBE_CHAINS
+#define KVX_PROBE_CHAINS 4
+#endif
+constexpr int kProbeChains = KVX_PROBE_CHAINS;  // per lane -> 32 x this query keys per warp step
 
 __device__ __forceinline__ unsigned long long pack_best(int64_t len, int32_t id) {
   // Larger len wins; on equal len the LOWER id must win, so store ~ordered(id).
