@@ -82,7 +82,10 @@ int64_t kvx_chain_hash(int64_t prev_key, uint64_t content_hash);
  * of d_tokens; its ceil(len/bs) keys go to d_keys[key_off[r] ...].
  * content_i = fold(chain_hash, block tokens as uint32, from 0);
  * key_i = chain_hash(key_{i-1}, content_i), key_{-1} = 0; the last block may
- * be partial.  d_key_off must be the exclusive scan of ceil(len/bs). */
+ * be partial.  d_key_off must be the exclusive scan of ceil(len/bs).
+ * Block sizes that are multiples of 16 with a 16-byte aligned d_tokens run the
+ * half-warp kernel (requests must be < 2^30 tokens each); others the
+ * producer / fold kernel.  Both are bit-identical. */
 int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req,
                          int64_t bs, const int64_t* d_key_off, int64_t* d_keys, void* stream);
 

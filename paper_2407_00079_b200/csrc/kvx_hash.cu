@@ -662,7 +662,9 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
     const size_t smem = std::max(hw::kMinCtaSmem, warps * per_warp);
     {
       std::lock_guard<std::mutex> lk(W.mu);
-      if (n_req <= hw::kOrderMaxReq && W.order_cap[dev] < n_req) {
+      int64_t order_max = hw::kOrderMaxReq;
+      if (const char* e = std::getenv("KVX_HASH_ORDER_MAX")) order_max = std::atoll(e);  // tests
+      if (n_req <= order_max && W.order_cap[dev] < n_req) {
         if (W.order[dev]) KVX_CUDA(cudaFree(W.order[dev]));
         W.order[dev] = nullptr;
         W.order_cap[dev] = 0;
@@ -670,7 +672,7 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
         KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&W.order[dev]), cap * sizeof(int32_t)));
         W.order_cap[dev] = cap;
       }
-      if (n_req <= hw::kOrderMaxReq) order = W.order[dev];
+      if (n_req <= order_max) order = W.order[dev];
       if (!W.hw_attr[dev]) {
         KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,

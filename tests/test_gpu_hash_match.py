@@ -214,3 +214,30 @@ def test_match_long_requests_and_empty(kvx, oracle_lib):
                                           _t(key_off, torch.int64))
     assert lens[:, 0].cpu().tolist() == [19000, 0, 63, 64, 65, 19000, 1]
     assert bi.cpu().tolist() == [9] * len(reqs)
+
+
+def test_block_hash_dispatch_paths(kvx, oracle_lib, monkeypatch):
+    """The bs % 16 == 0 kernel with the longest-first order, in index order
+    (batches above the order limit), and the any-alignment kernel that a
+    token pointer off 16 bytes falls back to: all bit-identical."""
+    rng = np.random.default_rng(5)
+    lens = rng.integers(0, 3000, size=300)
+    lens[7] = 0
+    tok_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    tokens = rng.integers(0, 32000, size=int(tok_off[-1]) + 8).astype(np.int32)
+    want, _ = oracle_lib.block_hash_batch(tokens, tok_off, 32)
+    t = _t(tokens, torch.int32)
+    off = _t(tok_off, torch.int64)
+    keys, _ = kvx.chain_hash_batch(t, off, 32)
+    assert np.array_equal(keys.cpu().numpy(), want)
+    monkeypatch.setenv("KVX_HASH_ORDER_MAX", "10")  # 300 requests > 10: index order
+    keys, _ = kvx.chain_hash_batch(t, off, 32)
+    assert np.array_equal(keys.cpu().numpy(), want)
+    monkeypatch.delenv("KVX_HASH_ORDER_MAX")
+    # token pointer 4 bytes past a 16-byte boundary: the fused any-alignment kernel
+    big = _t(np.concatenate([[0], tokens]), torch.int32)
+    keys, _ = kvx.chain_hash_batch(big[1:], off, 32)
+    assert np.array_equal(keys.cpu().numpy(), want)
+    monkeypatch.setenv("KVX_HASH_KERNEL", "fused")
+    keys, _ = kvx.chain_hash_batch(t, off, 32)
+    assert np.array_equal(keys.cpu().numpy(), want)
