@@ -41,7 +41,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "kvx_common.cuh"
 
@@ -600,12 +602,19 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
 }
 }  // namespace hw
 
+// Claim counters and the longest-first order are per (device, stream):
+// batches on different streams of one device run concurrently without
+// sharing them, batches on one stream are ordered by the stream.
+struct Scratch {
+  unsigned long long* ws = nullptr;  // 3 + SM count counters
+  int32_t* order = nullptr;
+  int64_t order_cap = 0;
+};
+
 struct Workspace {
   std::mutex mu;
-  unsigned long long* ws[64] = {nullptr};
+  std::map<std::pair<int, void*>, Scratch> scratch;
   int grid[64] = {0};
-  int32_t* order[64] = {nullptr};
-  int64_t order_cap[64] = {0};
   bool hw_attr[64] = {false};
 };
 
@@ -633,19 +642,19 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
   Workspace& W = workspace();
   unsigned long long* ws;
   int grid;
-  {
-    std::lock_guard<std::mutex> lk(W.mu);
-    if (!W.ws[dev]) {
-      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&W.ws[dev]),
-                          (3 + sm_count(dev)) * sizeof(unsigned long long)));
-      int per_sm = 0;
-      KVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_hash_fused_kernel,
-                                                             kHashThreads, 0));
-      W.grid[dev] = std::max(1, per_sm) * sm_count(dev);
-    }
-    ws = W.ws[dev];
-    grid = W.grid[dev];
+  std::lock_guard<std::mutex> lk(W.mu);  // host bookkeeping only; launches are async
+  Scratch& X = W.scratch[{dev, stream}];
+  if (!X.ws)
+    KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&X.ws),
+                        (3 + sm_count(dev)) * sizeof(unsigned long long)));
+  if (!W.grid[dev]) {
+    int per_sm = 0;
+    KVX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, block_hash_fused_kernel,
+                                                           kHashThreads, 0));
+    W.grid[dev] = std::max(1, per_sm) * sm_count(dev);
   }
+  ws = X.ws;
+  grid = W.grid[dev];
   // Block sizes that are multiples of 16 (every configuration the bench and the
   // reference's workloads use): the half-warp kernel.  KVX_HASH_KERNEL=fused
   // selects the producer/fold kernel for comparison.
@@ -660,25 +669,22 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
     const size_t per_warp = sizeof(hw::WarpSmem<1>);
     warps = std::min<int>(warps, static_cast<int>(hw::kMaxCtaSmem / per_warp));
     const size_t smem = std::max(hw::kMinCtaSmem, warps * per_warp);
-    {
-      std::lock_guard<std::mutex> lk(W.mu);
-      int64_t order_max = hw::kOrderMaxReq;
-      if (const char* e = std::getenv("KVX_HASH_ORDER_MAX")) order_max = std::atoll(e);  // tests
-      if (n_req <= order_max && W.order_cap[dev] < n_req) {
-        if (W.order[dev]) KVX_CUDA(cudaFree(W.order[dev]));
-        W.order[dev] = nullptr;
-        W.order_cap[dev] = 0;
-        const int64_t cap = std::max<int64_t>(n_req, 4096);
-        KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&W.order[dev]), cap * sizeof(int32_t)));
-        W.order_cap[dev] = cap;
-      }
-      if (n_req <= order_max) order = W.order[dev];
-      if (!W.hw_attr[dev]) {
-        KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(hw::kMaxCtaSmem)));
-        W.hw_attr[dev] = true;
-      }
+    int64_t order_max = hw::kOrderMaxReq;
+    if (const char* e = std::getenv("KVX_HASH_ORDER_MAX")) order_max = std::atoll(e);  // tests
+    if (n_req <= order_max && X.order_cap < n_req) {
+      if (X.order) KVX_CUDA(cudaFree(X.order));  // cudaFree waits for the device
+      X.order = nullptr;
+      X.order_cap = 0;
+      const int64_t cap = std::max<int64_t>(n_req, 4096);
+      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&X.order), cap * sizeof(int32_t)));
+      X.order_cap = cap;
+    }
+    if (n_req <= order_max) order = X.order;
+    if (!W.hw_attr[dev]) {
+      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(hw::kMaxCtaSmem)));
+      W.hw_attr[dev] = true;
     }
     if (order) {
       hw::order_kernel<<<1, 1024, 0, s>>>(d_key_off, n_req, order, ws + 1);  // also zeroes ws[1]

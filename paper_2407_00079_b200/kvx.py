@@ -189,6 +189,14 @@ def _stream(stream=None) -> int:
     return stream.cuda_stream
 
 
+def _torch_stream(stream, device) -> torch.cuda.Stream:
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if isinstance(stream, int):
+        return torch.cuda.ExternalStream(stream, device=device)
+    return stream
+
+
 def _ptr(t: Optional[torch.Tensor]):
     if t is None:
         return None
@@ -229,11 +237,13 @@ def chain_hash_batch(tokens: torch.Tensor, tok_off: torch.Tensor, bs: int,
     """Prefix-chained block keys of a batch of requests (K1).  Returns
     (keys, key_off).  tokens int32, tok_off int64 (n_req+1), both on the GPU."""
     assert tokens.dtype == torch.int32 and tok_off.dtype == torch.int64
-    if key_off is None:
-        key_off = key_offsets(tok_off, bs)
-    if keys is None:
-        n_keys = int(key_off[-1].item())
-        keys = torch.empty(max(n_keys, 1), dtype=torch.int64, device=tokens.device)[:n_keys]
+    # the offsets and the output are made on the stream the kernel runs on
+    with torch.cuda.stream(_torch_stream(stream, tokens.device)):
+        if key_off is None:
+            key_off = key_offsets(tok_off, bs)
+        if keys is None:
+            n_keys = int(key_off[-1].item())
+            keys = torch.empty(max(n_keys, 1), dtype=torch.int64, device=tokens.device)[:n_keys]
     check(_L.kvx_chain_hash_batch(_ptr(tokens) if tokens.numel() else None, _ptr(tok_off),
                                   len(tok_off) - 1, bs, _ptr(key_off),
                                   _ptr(keys) if keys.numel() else None, _stream(stream)))

@@ -241,3 +241,25 @@ def test_block_hash_dispatch_paths(kvx, oracle_lib, monkeypatch):
     monkeypatch.setenv("KVX_HASH_KERNEL", "fused")
     keys, _ = kvx.chain_hash_batch(t, off, 32)
     assert np.array_equal(keys.cpu().numpy(), want)
+
+
+def test_block_hash_concurrent_streams(kvx, oracle_lib):
+    """Two batches in flight on two streams of one device (their claim
+    counters and orders must not be shared): both bit-exact."""
+    rng = np.random.default_rng(11)
+    batches = []
+    for n in (500, 700):
+        lens = rng.integers(0, 4000, size=n)
+        tok_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        tokens = rng.integers(0, 32000, size=int(tok_off[-1])).astype(np.int32)
+        want, _ = oracle_lib.block_hash_batch(tokens, tok_off, 16)
+        batches.append((_t(tokens, torch.int32), _t(tok_off, torch.int64), want))
+    streams = [torch.cuda.Stream(DEV), torch.cuda.Stream(DEV)]
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(3):
+        for (t, off, _w), st in zip(batches, streams):
+            outs.append(kvx.chain_hash_batch(t, off, 16, stream=st)[0])
+    torch.cuda.synchronize()
+    for i, k in enumerate(outs):
+        assert np.array_equal(k.cpu().numpy(), batches[i % 2][2])
