@@ -56,6 +56,9 @@ def parse_args():
                          "512 MiB per layer; 16 for config 3, whose 2048-token chunks are only "
                          "8 MiB per layer and launch-overhead bound one layer at a time)")
     ap.add_argument("--ring", type=int, default=3)
+    ap.add_argument("--graph", action="store_true",
+                    help="local_fused: record one step's launches as a CUDA graph and replay it "
+                         "every step (for launch-bound small units)")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3],
                     help="1: one 8K request; 2: 64 x 8K requests, 50%% shared prefix "
                          "(default); 3: one 128K request")
@@ -397,9 +400,14 @@ def run_kvx(args):
         else:
             st.send(dev_src[w], dev_dst[w], lo, hi, chunk, args.layers_per_chunk)
 
+    graph = {"on": False}
+
     def step():
-        for u in plan["units"]:
-            run_unit(u)
+        if graph["on"]:
+            st.replay()
+        else:
+            for u in plan["units"]:
+                run_unit(u)
         st.finish()
 
     st.after(main)
@@ -431,10 +439,29 @@ def run_kvx(args):
         raise SystemExit(f"PARITY FAILURE: {bad} mismatched 64-bit words")
 
     # ---- timed region: CUDA events on the streamer's queue, max over ranks
-    # time a sample of the dominant launches -- every 4th (every 16th for the
-    # small Config 3 units): an event pair costs ~µs of host time and sits in
-    # the timed region
-    st.set_timing(True, 16 if args.config == 3 else 4)
+    # time a sample of the dominant launches, ~16 per step: an event pair costs
+    # ~µs of host time, sits in the timed region and serialises the
+    # programmatic-dependent launches around it
+    def n_units(w, lo, hi, chunk):
+        n = max(1, len(host_src[w]))
+        return -(-n // (chunk or n)) * -(-(hi - lo) // args.layers_per_chunk)
+
+    units_per_step = sum(n_units(*u) for u in plan["units"])
+    st.set_timing(True, max(4, units_per_step // 16))
+    if args.graph:
+        if mode != "local_fused":
+            raise SystemExit("--graph needs the local_fused mode")
+        # one step's launches (and the sampled event pairs) become a CUDA graph
+        st.after(main)
+        st.record_begin()
+        for u in plan["units"]:
+            run_unit(u)
+        st.record_end()
+        graph["on"] = True
+        for _ in range(2):
+            step()
+        st.finish(main)
+        torch.cuda.synchronize()
     st.launch_stats(reset=True)
     clocks = ClockSampler(dev)
     clocks.start()
@@ -444,6 +471,7 @@ def run_kvx(args):
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
     e0.record(main)
     st.after(main)
     for _ in range(args.steps):
@@ -451,12 +479,14 @@ def run_kvx(args):
     st.finish(main)
     e1.record(main)
     torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - w0) * 1e3  # host clock, device idle at both ends
     barrier()
     launches = pkg.launch_count() - launches0
     clk = clocks.stop()
     st.set_timing(False)
     ksum = st.launch_stats(reset=True)
     ms_total = max_over_ranks(e0.elapsed_time(e1), d)
+    wall_step = max_over_ranks(wall_ms, d) / args.steps  # cross-check of the event clock
     launches_all = int(sum_over_ranks(float(launches), d))
     payload = plan["payload_total"]
     value = payload * args.steps / (ms_total / 1e3) / GB
@@ -542,10 +572,12 @@ def run_kvx(args):
             "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
             "higher_is_better": True, "scaling": plan["scaling"], "vs_baseline": None,
+            "host_wall_ms_per_step": wall_step,
             "dtype": "u8",
             "data": "synthetic (counter-based splitmix64 KV content; generate_workload block ids)",
             "config": {**plan["describe"], "config": args.config, "mode": mode,
                        "copy_impl": args.copy_impl, "layers_per_chunk": args.layers_per_chunk,
+                       "cuda_graph": bool(args.graph),
                        "pairs": role.pairs,
                        "parallelism": ("local (prefill+decode on one GPU)" if world == 1 else
                                        f"{role.pairs}P->{role.pairs}D pairs"),

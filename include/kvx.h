@@ -344,6 +344,14 @@ int kvx_streamer_set_timing(kvx_streamer* s, int on, int stride);
 int kvx_streamer_launch_stats(kvx_streamer* s, int64_t* launches, double* avg_ms,
                               double* avg_bytes, int reset);
 uint64_t kvx_streamer_units(const kvx_streamer* s);
+/* CUDA-graph record / replay of one step (LOCAL_FUSED only): the sends issued
+ * between record_begin and record_end are captured, not run; each replay runs
+ * them again with one cudaGraphLaunch on the streamer's queue (tables are read
+ * at replay time; same pointers and ranges).  Call finish(stream) after
+ * record_end, not inside the recording. */
+int kvx_streamer_record_begin(kvx_streamer* s);
+int kvx_streamer_record_end(kvx_streamer* s);
+int kvx_streamer_replay(kvx_streamer* s);
 
 /* ---- KVCache store of one instance + migration (hot-spot replication) ---- */
 

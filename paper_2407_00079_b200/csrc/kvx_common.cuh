@@ -47,6 +47,7 @@ __host__ __device__ __forceinline__ bool is_reserved(int64_t k) { return k <= kK
 int set_error(int status, const std::string& msg);
 int cuda_error(cudaError_t e, const char* where);
 void count_launch(uint64_t n = 1);
+void uncount_launches(uint64_t n);  // launches recorded into a graph, not run
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -65,6 +66,13 @@ struct DeviceGuard {
 };
 
 int sm_count(int dev);
+
+// kvx_copy_paged whose launch may overlap the previous kernel on the stream
+// (programmatic dependent launch): only for copies independent of it, e.g.
+// the streamer's layer-wise units, which touch disjoint (chunk, layer) slabs.
+int copy_paged_overlapped(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
+                          const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi,
+                          void* stream);
 
 }  // namespace kvx
 

@@ -180,6 +180,10 @@ __device__ __forceinline__ void lsu_copy(const SlabCopy& c) {
 
 template <class Idx>
 __global__ void __launch_bounds__(kLsuThreads, 2) copy_lsu_kernel(const SlabCopy c) {
+  // A launch made with programmatic stream serialization (the streamer's
+  // independent layer-wise units) lets the next unit's CTAs start now; with
+  // no programmatic dependent this is a no-op.
+  asm volatile("griddepcontrol.launch_dependents;");
   lsu_copy<true, true, Idx>(c);
 }
 
@@ -310,6 +314,8 @@ int launch_tma(const SlabCopy& c, int dev, int ctas_per_sm, cudaStream_t s) {
   return KVX_OK;
 }
 
+thread_local bool t_overlap_prev = false;  // set by copy_paged_overlapped
+
 int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
   const int64_t units = c.planes * c.n;
   if (units == 0 || c.slab == 0) return KVX_OK;
@@ -343,9 +349,29 @@ int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
       const char* e = std::getenv("KVX_LSU_VARIANT");  // measurement knob
       return e ? std::atoi(e) : 0;
     }();
-    if (variant == 1) copy_lsu_plain_kernel<<<blocks, kLsuThreads, 0, s>>>(c);
-    else if (items + blocks < (int64_t{1} << 32)) copy_lsu_kernel<uint32_t><<<blocks, kLsuThreads, 0, s>>>(c);
-    else copy_lsu_kernel<int64_t><<<blocks, kLsuThreads, 0, s>>>(c);
+    if (variant == 1) {
+      copy_lsu_plain_kernel<<<blocks, kLsuThreads, 0, s>>>(c);
+    } else if (t_overlap_prev) {
+      // programmatic dependent launch: this copy may start while the previous
+      // kernel on the stream is still running (caller guarantees independence)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(blocks);
+      cfg.blockDim = dim3(kLsuThreads);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (items + blocks < (int64_t{1} << 32))
+        KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_lsu_kernel<uint32_t>, c));
+      else
+        KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_lsu_kernel<int64_t>, c));
+    } else if (items + blocks < (int64_t{1} << 32)) {
+      copy_lsu_kernel<uint32_t><<<blocks, kLsuThreads, 0, s>>>(c);
+    } else {
+      copy_lsu_kernel<int64_t><<<blocks, kLsuThreads, 0, s>>>(c);
+    }
     KVX_LAUNCH_CHECK("copy_lsu_kernel");
   }
   return KVX_OK;
@@ -600,6 +626,21 @@ int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* ds
   DeviceGuard g(src->d.device);
   return launch_copy(c, src->d.device, as_stream(stream));
 }
+
+}  // extern "C"
+
+namespace kvx {
+int copy_paged_overlapped(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
+                          const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi,
+                          void* stream) {
+  t_overlap_prev = true;
+  const int rc = kvx_copy_paged(src, d_src_table, dst, d_dst_table, n, lo, hi, stream);
+  t_overlap_prev = false;
+  return rc;
+}
+}  // namespace kvx
+
+extern "C" {
 
 int kvx_copy_check(void* stream) {
   KVX_CUDA(cudaStreamSynchronize(as_stream(stream)));

@@ -35,6 +35,7 @@ int cuda_error(cudaError_t e, const char* where) {
 }
 
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void uncount_launches(uint64_t n) { g_launches.fetch_sub(n, std::memory_order_relaxed); }
 
 int sm_count(int dev) {
   static std::mutex mu;

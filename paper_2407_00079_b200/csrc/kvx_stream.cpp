@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -59,6 +60,13 @@ struct kvx_streamer {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
   std::vector<double> timed_bytes;
   size_t timed_used = 0;
+  // CUDA-graph record / replay of one step (LOCAL_FUSED): the units of the
+  // sends between record_begin and record_end become kernel nodes of one graph
+  bool recording = false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  uint64_t graph_launches = 0, graph_units = 0, rec_launch0 = 0, rec_seq0 = 0;
+  size_t graph_timed = 0;  // timed pairs [0, graph_timed) are graph nodes (re-recorded per replay)
 };
 
 namespace {
@@ -76,24 +84,40 @@ int ev_pair(kvx_streamer* s, cudaEvent_t* a, cudaEvent_t* b) {
   return KVX_OK;
 }
 
+// Whether the next dominant launch will be bracketed by timing events.
+bool will_sample(const kvx_streamer* s) {
+  return s->timing && (s->timing_count % s->timing_stride == 0);
+}
+
 // Wrap one dominant launch with timing events when enabled.
 template <class F>
 int timed_launch(kvx_streamer* s, cudaStream_t st, double bytes, F&& launch) {
   cudaEvent_t a = nullptr, b = nullptr;
   const bool on = s->timing && (s->timing_count++ % s->timing_stride == 0);
+  // while recording a graph the pair becomes two event-record nodes that
+  // re-record on every replay
+  const unsigned flags = s->recording ? cudaEventRecordExternal : cudaEventRecordDefault;
   if (on) {
     int rc = ev_pair(s, &a, &b);
     if (rc) return rc;
-    KVX_CUDA(cudaEventRecord(a, st));
+    KVX_CUDA(cudaEventRecordWithFlags(a, st, flags));
   }
   int rc = launch();
   if (rc) return rc;
   if (on) {
-    KVX_CUDA(cudaEventRecord(b, st));
+    KVX_CUDA(cudaEventRecordWithFlags(b, st, flags));
     s->timed_bytes[s->timed_used] = bytes;
     ++s->timed_used;
   }
   return KVX_OK;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("KVX_STREAM_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 bool is_peer(const kvx_streamer* s) {
@@ -181,6 +205,13 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
 int kvx_streamer_destroy(kvx_streamer* s) {
   if (!s) return KVX_OK;
   kvx::DeviceGuard g(s->device);
+  if (s->recording) {
+    cudaGraph_t dropped = nullptr;
+    cudaStreamEndCapture(s->s_main, &dropped);
+    if (dropped) cudaGraphDestroy(dropped);
+  }
+  if (s->graph_exec) cudaGraphExecDestroy(s->graph_exec);
+  if (s->graph) cudaGraphDestroy(s->graph);
   if (s->s_main) cudaStreamSynchronize(s->s_main);
   if (s->s_second) cudaStreamSynchronize(s->s_second);
   if (s->xfer) kvx_xfer_destroy(s->xfer);
@@ -290,6 +321,7 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
   kvx::DeviceGuard g(s->device);
   const int64_t slab = kvx_pool_slab_bytes(s->src);
   const int R = static_cast<int>(s->ring.size());
+  bool first_unit = true;
   for (int64_t b0 = 0; b0 < n; b0 += chunk_blocks) {
     const int64_t nb = std::min(chunk_blocks, n - b0);
     for (int32_t l0 = layer_lo; l0 < layer_hi; l0 += layers_per_chunk) {
@@ -298,12 +330,22 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
       const uint64_t c = s->seq++;
       int rc = KVX_OK;
       switch (s->d.mode) {
-        case KVX_STREAM_LOCAL_FUSED:
+        case KVX_STREAM_LOCAL_FUSED: {
+          // The units of ONE send touch disjoint (chunk, layer) slabs, so each
+          // unit after the first may overlap its predecessor (programmatic
+          // dependent launch; KVX_STREAM_PDL=0: off).  The first unit of a
+          // call waits for everything before it (an earlier send may have
+          // written the same decode slots), and a launch sampled for timing
+          // runs isolated so its duration is its own.
+          const bool overlap = pdl_enabled() && !first_unit && !will_sample(s);
           rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
-            return kvx_copy_paged(s->src, d_src_table + b0, s->dst, d_dst_table + b0, nb, l0, l1,
-                                  s->s_main);
+            return overlap ? kvx::copy_paged_overlapped(s->src, d_src_table + b0, s->dst,
+                                                        d_dst_table + b0, nb, l0, l1, s->s_main)
+                           : kvx_copy_paged(s->src, d_src_table + b0, s->dst, d_dst_table + b0,
+                                            nb, l0, l1, s->s_main);
           });
           break;
+        }
         case KVX_STREAM_PEER_PULL:
           // the KV of unit c is in the pool once the work queued so far on the
           // sender's queue (the prefill of that layer, in a serving engine) is done
@@ -358,6 +400,7 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
           return set_error(KVX_EINVAL, "kvx_streamer_send: bad mode");
       }
       if (rc) return rc;
+      first_unit = false;
     }
   }
   return KVX_OK;
@@ -466,7 +509,62 @@ int kvx_streamer_launch_stats(kvx_streamer* s, int64_t* launches, double* avg_ms
   *launches = static_cast<int64_t>(s->timed_used);
   *avg_ms = s->timed_used ? ms_sum / s->timed_used : 0.0;
   *avg_bytes = s->timed_used ? bytes_sum / s->timed_used : 0.0;
-  if (reset) s->timed_used = 0;
+  if (reset) s->timed_used = s->graph_timed;  // a recorded graph keeps its pairs
+  return KVX_OK;
+}
+
+// ---- CUDA-graph record / replay (LOCAL_FUSED) ------------------------------
+// A step of fine-grained layer-wise units (Config 3 at one 2,048-token chunk
+// x one layer = 8 MiB per unit: 5,120 launches) is bound by host launch cost.
+// Record the step's sends once as a graph, then replay it: one
+// cudaGraphLaunch per step.  The tables are read at replay time, so their
+// contents may change between replays (same device pointers and ranges).
+int kvx_streamer_record_begin(kvx_streamer* s) {
+  KVX_REQUIRE(s && s->d.mode == KVX_STREAM_LOCAL_FUSED,
+              "kvx_streamer_record_begin: graph record/replay is for the local fused mode");
+  KVX_REQUIRE(!s->recording, "kvx_streamer_record_begin: already recording");
+  kvx::DeviceGuard g(s->device);
+  if (s->graph_exec) KVX_CUDA(cudaGraphExecDestroy(s->graph_exec));
+  if (s->graph) KVX_CUDA(cudaGraphDestroy(s->graph));
+  s->graph_exec = nullptr;
+  s->graph = nullptr;
+  s->graph_timed = 0;
+  s->timed_used = 0;
+  s->rec_launch0 = kvx_launch_count();
+  s->rec_seq0 = s->seq;
+  KVX_CUDA(cudaStreamBeginCapture(s->s_main, cudaStreamCaptureModeRelaxed));
+  s->recording = true;
+  return KVX_OK;
+}
+
+int kvx_streamer_record_end(kvx_streamer* s) {
+  KVX_REQUIRE(s && s->recording, "kvx_streamer_record_end: not recording");
+  kvx::DeviceGuard g(s->device);
+  s->recording = false;
+  cudaGraph_t graph = nullptr;
+  KVX_CUDA(cudaStreamEndCapture(s->s_main, &graph));
+  cudaError_t e = cudaGraphInstantiate(&s->graph_exec, graph, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(graph);
+    s->graph_exec = nullptr;
+    return kvx::cuda_error(e, "kvx_streamer_record_end: cudaGraphInstantiate");
+  }
+  s->graph = graph;
+  // the recorded units have not run: launches and units count on replay
+  s->graph_launches = kvx_launch_count() - s->rec_launch0;
+  kvx::uncount_launches(s->graph_launches);
+  s->graph_units = s->seq - s->rec_seq0;
+  s->seq = s->rec_seq0;
+  s->graph_timed = s->timed_used;
+  return KVX_OK;
+}
+
+int kvx_streamer_replay(kvx_streamer* s) {
+  KVX_REQUIRE(s && s->graph_exec && !s->recording, "kvx_streamer_replay: nothing recorded");
+  kvx::DeviceGuard g(s->device);
+  KVX_CUDA(cudaGraphLaunch(s->graph_exec, s->s_main));
+  kvx::count_launch(s->graph_launches);
+  s->seq += s->graph_units;
   return KVX_OK;
 }
 

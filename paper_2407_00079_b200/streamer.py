@@ -51,6 +51,9 @@ _sig("kvx_streamer_set_timing", C.c_int, _vp, C.c_int, C.c_int)
 _sig("kvx_streamer_launch_stats", C.c_int, _vp, C.POINTER(_i64), C.POINTER(C.c_double),
      C.POINTER(C.c_double), C.c_int)
 _sig("kvx_streamer_units", C.c_uint64, _vp)
+_sig("kvx_streamer_record_begin", C.c_int, _vp)
+_sig("kvx_streamer_record_end", C.c_int, _vp)
+_sig("kvx_streamer_replay", C.c_int, _vp)
 
 
 class Streamer:
@@ -126,6 +129,17 @@ class Streamer:
     @property
     def units(self) -> int:
         return int(_L.kvx_streamer_units(self.h))
+
+    def record_begin(self):
+        """Capture the following sends (local fused mode) into a CUDA graph."""
+        check(_L.kvx_streamer_record_begin(self.h))
+
+    def record_end(self):
+        check(_L.kvx_streamer_record_end(self.h))
+
+    def replay(self):
+        """Run the recorded step again: one cudaGraphLaunch."""
+        check(_L.kvx_streamer_replay(self.h))
 
 
 class NcclStreamer:

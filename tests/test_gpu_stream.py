@@ -48,6 +48,69 @@ def test_local_streamer_vs_oracle(kvx, oracle_lib, mode, chunk, lpc):
     assert s.units == units
 
 
+def test_local_streamer_graph_replay(kvx, oracle_lib):
+    """Record one step of many small units (programmatic-dependent launches)
+    as a CUDA graph, replay it: bit-exact, and the tables are read at replay
+    time (new contents, same pointers)."""
+    from paper_2407_00079_b200.streamer import Streamer
+    L, bs, n = 6, 16, 23
+    src = kvx.KVPool(L, bs, 8, 128, 2, 40, 0)
+    dst = kvx.KVPool(L, bs, 8, 128, 2, 50, 0)
+    src.fill_synthetic(4)
+    rng = np.random.default_rng(3)
+    st_d = _t(rng.integers(0, 40, size=n).astype(np.int32))
+    dt_d = _t(rng.permutation(50)[:n].astype(np.int32))
+    s = Streamer("local_fused", "local", src, dst)
+    s.send(st_d, dt_d, 0, L, 2, 1)  # eager warm-up: 12 chunks x 6 layers
+    s.finish(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    u0 = s.units
+    launches0 = kvx.launch_count()
+    s.record_begin()
+    s.send(st_d, dt_d, 0, L, 2, 1)
+    s.record_end()
+    assert s.units == u0 and kvx.launch_count() == launches0  # recorded, not run
+    o = oracle_lib
+    for trial in range(2):
+        st_tab = rng.integers(0, 40, size=n).astype(np.int32)
+        dt_tab = rng.permutation(50)[:n].astype(np.int32)
+        st_d.copy_(_t(st_tab))
+        dt_d.copy_(_t(dt_tab))
+        dst.tensor_view().zero_()
+        torch.cuda.synchronize()
+        s.replay()
+        s.finish(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        want = np.zeros(dst.nbytes, dtype=np.uint8)
+        o.copy_paged(src.tensor_view().cpu().numpy(), 40, st_tab, want, 50, dt_tab, src.slab,
+                     0, L)
+        assert np.array_equal(dst.tensor_view().cpu().numpy(), want), trial
+    assert s.units == u0 + 2 * 12 * 6
+    assert kvx.launch_count() == launches0 + 2 * 12 * 6
+
+
+def test_local_streamer_calls_stay_ordered(kvx, oracle_lib):
+    """Units inside one send overlap (programmatic dependent launch); a later
+    send that rewrites the same decode slots must still land after it."""
+    from paper_2407_00079_b200.streamer import Streamer
+    L, bs, n = 8, 16, 64
+    src = kvx.KVPool(L, bs, 8, 128, 2, 200, 0)
+    dst = kvx.KVPool(L, bs, 8, 128, 2, 64, 0)
+    src.fill_synthetic(9)
+    s = Streamer("local_fused", "local", src, dst)
+    dt_tab = np.arange(n, dtype=np.int32)
+    rng = np.random.default_rng(8)
+    tabs = [rng.permutation(200)[:n].astype(np.int32) for _ in range(6)]
+    for t in tabs:  # six waves into the same 64 slots, one layer per unit
+        s.send(_t(t), _t(dt_tab), 0, L, 16, 1)
+    s.finish(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    want = np.zeros(dst.nbytes, dtype=np.uint8)
+    oracle_lib.copy_paged(src.tensor_view().cpu().numpy(), 200, tabs[-1], want, 64, dt_tab,
+                          src.slab, 0, L)
+    assert np.array_equal(dst.tensor_view().cpu().numpy(), want)
+
+
 def test_streamer_rejects_bad_shapes(kvx):
     from paper_2407_00079_b200.streamer import Streamer
     src = kvx.KVPool(2, 16, 8, 128, 2, 8, 0)
