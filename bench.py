@@ -93,12 +93,20 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # nvidia-smi takes a moment to start sampling
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.05)
         except FileNotFoundError:
             self.proc = None
+        self.mark_at = 0
+
+    def mark(self):
+        """Start of the timed region: only later samples are reported."""
+        self.mark_at = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -115,7 +123,8 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        timed = self.lines[self.mark_at:] or self.lines[-2:]
+        for ln in timed:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -471,6 +480,7 @@ def run_kvx(args):
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark()
     w0 = time.perf_counter()
     e0.record(main)
     st.after(main)
