@@ -73,6 +73,12 @@ int sm_count(int dev);
 int copy_paged_overlapped(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
                           const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi,
                           void* stream);
+// Pull copy of a unit whose readiness flag is waited for inside the kernel
+// (d_flag >= value, system-scope acquire); with overlap_prev it may start
+// while the previous kernel on the stream runs (programmatic dependent launch).
+int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
+                    const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, void* stream,
+                    const uint64_t* d_flag, uint64_t value, bool overlap_prev);
 
 }  // namespace kvx
 

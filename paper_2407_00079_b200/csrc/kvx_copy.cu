@@ -50,12 +50,26 @@ struct SlabCopy {
 // Set when a table entry outside [0, slots) was met (that block is skipped,
 // not copied), per device; kvx_copy_check() reports and clears it.
 __device__ unsigned long long g_bad_table_entries = 0;
+// Set when a pull copy gave up waiting for its readiness flag (kvx_copy_check).
+__device__ unsigned long long g_wait_timeouts = 0;
 
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+  return r;
+}
+
+// Coherent 16-B load (the pull copy reads a peer pool that another GPU
+// writes while the kernel may already be running: the read-only .nc path is
+// not ordered by the flag acquire).
+__device__ __forceinline__ int4 ld_coherent(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
   return r;
 }
 
@@ -125,7 +139,7 @@ __device__ __forceinline__ void st_stream(int4* p, const int4& v) {
 // Idx: uint32_t when the launch has < 2^32 work items (the host checks), so
 // the per-item index arithmetic is 32-bit (64-bit division is a long
 // subroutine that also cost the kernel register spills).
-template <bool kCsStores, bool kPipelined, class Idx>
+template <bool kCsStores, bool kPipelined, class Idx, bool kCoherent = false>
 __device__ __forceinline__ void lsu_copy(const SlabCopy& c) {
   const Idx parts = static_cast<Idx>((c.slab + kLsuItem - 1) / kLsuItem);
   const Idx items = static_cast<Idx>(c.planes * c.n * parts);
@@ -144,7 +158,7 @@ __device__ __forceinline__ void lsu_copy(const SlabCopy& c) {
 #pragma unroll
     for (int j = 0; j < kLsuUnroll; ++j) {
       const int v = threadIdx.x + j * kLsuThreads;
-      if (v < n) buf[j] = ld_stream(sv + v);
+      if (v < n) buf[j] = kCoherent ? ld_coherent(sv + v) : ld_stream(sv + v);
     }
   };
   auto store = [&](const int4 (&buf)[kLsuUnroll], int n, int4* dst) {
@@ -185,6 +199,39 @@ __global__ void __launch_bounds__(kLsuThreads, 2) copy_lsu_kernel(const SlabCopy
   // no programmatic dependent this is a no-op.
   asm volatile("griddepcontrol.launch_dependents;");
   lsu_copy<true, true, Idx>(c);
+}
+
+// Pull copy of one layer-wise unit whose readiness flag is checked in the
+// kernel (PEER_PULL receiver): thread 0 waits until the sender's flag reaches
+// `value` (system-scope acquire; the sender's stream write fences the unit's
+// KV first), the CTA follows through the barrier, and only then are
+// dependents released -- so with programmatic dependent launch at most the
+// next unit waits ahead of the data.  Gives up after 20 s (g_wait_timeouts;
+// kvx_copy_check reports it) instead of hanging the GPU.
+template <class Idx>
+__global__ void __launch_bounds__(kLsuThreads, 2) copy_pull_kernel(
+    const SlabCopy c, const unsigned long long* __restrict__ flag, unsigned long long value) {
+  __shared__ int go;
+  if (threadIdx.x == 0) {
+    unsigned long long t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int ok = 1;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      if (v >= value) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) {
+        ok = 0;
+        g_wait_timeouts = 1;
+        break;
+      }
+      __nanosleep(256);
+    }
+    go = ok;
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (go) lsu_copy<true, true, Idx, true>(c);
 }
 
 // ---- TMA bulk-copy pipeline ----------------------------------------------
@@ -630,6 +677,51 @@ int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* ds
 }  // extern "C"
 
 namespace kvx {
+int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
+                    const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, void* stream,
+                    const uint64_t* d_flag, uint64_t value, bool overlap_prev) {
+  int st = check_range(src, n, lo, hi);
+  if (st) return st;
+  st = check_range(dst, n, lo, hi);
+  if (st) return st;
+  KVX_REQUIRE(src->slab == dst->slab, "copy_paged_pull: slab sizes differ");
+  if (n == 0 || lo == hi) return KVX_OK;
+  KVX_REQUIRE(d_src_table && d_dst_table && d_flag, "copy_paged_pull: NULL argument");
+  SlabCopy c;
+  c.src = src->base + static_cast<int64_t>(lo) * 2 * src->d.slots * src->slab;
+  c.src_plane = src->d.slots * src->slab;
+  c.src_table = d_src_table;
+  c.dst = dst->base + static_cast<int64_t>(lo) * 2 * dst->d.slots * dst->slab;
+  c.dst_plane = dst->d.slots * dst->slab;
+  c.dst_table = d_dst_table;
+  c.n = n;
+  c.src_slots = static_cast<uint32_t>(src->d.slots);
+  c.dst_slots = static_cast<uint32_t>(dst->d.slots);
+  c.planes = static_cast<int64_t>(hi - lo) * 2;
+  c.slab = src->slab;
+  const int dev = dst->d.device;  // the pulling GPU
+  DeviceGuard g(dev);
+  const int64_t items = c.planes * c.n * ((c.slab + kLsuItem - 1) / kLsuItem);
+  const int blocks = static_cast<int>(std::min<int64_t>(items, static_cast<int64_t>(sm_count(dev)) * 4));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(kLsuThreads);
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = overlap_prev ? attr : nullptr;
+  cfg.numAttrs = overlap_prev ? 1 : 0;
+  const auto* f = reinterpret_cast<const unsigned long long*>(d_flag);
+  const unsigned long long v = value;
+  if (items + blocks < (int64_t{1} << 32))
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<uint32_t>, c, f, v));
+  else
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<int64_t>, c, f, v));
+  KVX_LAUNCH_CHECK("copy_pull_kernel");
+  return KVX_OK;
+}
+
 int copy_paged_overlapped(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
                           const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi,
                           void* stream) {
@@ -644,7 +736,12 @@ extern "C" {
 
 int kvx_copy_check(void* stream) {
   KVX_CUDA(cudaStreamSynchronize(as_stream(stream)));
-  unsigned long long bad = 0, zero = 0;
+  unsigned long long timeouts = 0, bad = 0, zero = 0;
+  KVX_CUDA(cudaMemcpyFromSymbol(&timeouts, g_wait_timeouts, sizeof(timeouts)));
+  if (timeouts) {
+    KVX_CUDA(cudaMemcpyToSymbol(g_wait_timeouts, &zero, sizeof(zero)));
+    return set_error(KVX_ECUDA, "kvx_copy_check: a pull copy timed out waiting for its unit");
+  }
   KVX_CUDA(cudaMemcpyFromSymbol(&bad, g_bad_table_entries, sizeof(bad)));
   if (bad == 0) return KVX_OK;
   KVX_CUDA(cudaMemcpyToSymbol(g_bad_table_entries, &zero, sizeof(zero)));

@@ -415,6 +415,7 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t
   kvx::DeviceGuard g(s->device);
   const int64_t slab = kvx_pool_slab_bytes(s->dst);
   const int R = static_cast<int>(s->ring.size());
+  bool first_unit = true;
   for (int64_t b0 = 0; b0 < n; b0 += chunk_blocks) {
     const int64_t nb = std::min(chunk_blocks, n - b0);
     for (int32_t l0 = layer_lo; l0 < layer_hi; l0 += layers_per_chunk) {
@@ -425,7 +426,22 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t
       KVX_REQUIRE(d_dst_table, "kvx_streamer_recv: NULL table");
       if (s->d.mode == KVX_STREAM_PEER_PULL) {
         KVX_REQUIRE(d_src_table && s->peer_view, "kvx_streamer_recv: pull needs the src table");
-        int rc = kvx_signal_wait(s->s_main, s->flag, c + 1);  // sender: unit c is ready
+        // After the first unit of a call, the pull kernel waits for the
+        // sender's flag itself and is launched programmatically dependent, so
+        // unit c+1 ramps up while unit c drains; the first unit (and a launch
+        // sampled for timing) waits on the stream instead and runs isolated.
+        const bool in_kernel = pdl_enabled() && !first_unit && !will_sample(s);
+        first_unit = false;
+        int rc = KVX_OK;
+        if (in_kernel) {
+          rc = timed_launch(s, s->s_main, 1.0 * payload, [&] {
+            return kvx::copy_paged_pull(s->peer_view, d_src_table + b0, s->dst, d_dst_table + b0,
+                                        nb, l0, l1, s->s_main, s->flag, c + 1, true);
+          });
+          if (rc) return rc;
+          continue;
+        }
+        rc = kvx_signal_wait(s->s_main, s->flag, c + 1);  // sender: unit c is ready
         if (rc) return rc;
         rc = timed_launch(s, s->s_main, 1.0 * payload, [&] {
           return kvx_copy_paged(s->peer_view, d_src_table + b0, s->dst, d_dst_table + b0, nb, l0,
