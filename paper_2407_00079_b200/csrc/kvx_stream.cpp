@@ -352,13 +352,18 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
           KVX_REQUIRE(s->peer_flag, "kvx_streamer_send: not connected");
           rc = kvx_signal_write(s->s_main, s->peer_flag, c + 1);
           break;
-        case KVX_STREAM_PEER_FUSED:
+        case KVX_STREAM_PEER_FUSED: {
           KVX_REQUIRE(s->peer_view, "kvx_streamer_send: not connected");
+          // disjoint (chunk, layer) slabs of the receiver's pool: as LOCAL_FUSED
+          const bool overlap = pdl_enabled() && !first_unit && !will_sample(s);
           rc = timed_launch(s, s->s_main, 1.0 * payload, [&] {
-            return kvx_copy_paged(s->src, d_src_table + b0, s->peer_view, d_dst_table + b0, nb,
-                                  l0, l1, s->s_main);
+            return overlap ? kvx::copy_paged_overlapped(s->src, d_src_table + b0, s->peer_view,
+                                                        d_dst_table + b0, nb, l0, l1, s->s_main)
+                           : kvx_copy_paged(s->src, d_src_table + b0, s->peer_view,
+                                            d_dst_table + b0, nb, l0, l1, s->s_main);
           });
           break;
+        }
         case KVX_STREAM_LOCAL_STAGED: {
           KVX_REQUIRE(payload <= s->d.slot_bytes, "kvx_streamer_send: unit larger than a slot");
           const int slot = static_cast<int>(c % R);
