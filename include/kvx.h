@@ -325,7 +325,13 @@ int kvx_streamer_connect(kvx_streamer* s, const uint8_t* blob, int64_t len,
                          const kvx_pool_desc* peer_pool);
 void* kvx_streamer_stream(kvx_streamer* s);
 /* Sender / local: enqueue n blocks (device tables; dst table unused by PEER_CE
- * senders) in units of chunk_blocks x layers_per_chunk. */
+ * senders) in units of chunk_blocks x layers_per_chunk.  The units of ONE call
+ * touch disjoint (chunk, layer) slabs and may run overlapped (programmatic
+ * dependent launch in LOCAL_FUSED / PEER_FUSED, and in the PEER_PULL
+ * receiver, whose pull kernels then wait for the sender's unit flag
+ * themselves); the first unit of a call waits for all earlier work on the
+ * streamer's queues, so successive calls stay ordered.  KVX_STREAM_PDL=0
+ * turns the overlap off.  A destination table must not repeat a slot. */
 int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t* d_dst_table,
                       int64_t n, int64_t chunk_blocks, int32_t layer_lo, int32_t layer_hi,
                       int32_t layers_per_chunk);

@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(1024) order_kernel(const int64_t* __restrict__
   __shared__ int hist[kOrderBuckets];
   __shared__ int part[1024];
   const int t = threadIdx.x;
+  asm volatile("griddepcontrol.launch_dependents;");  // the hash grid may get resident now
   for (int b = t; b < kOrderBuckets; b += blockDim.x) hist[b] = 0;
   if (t == 0) *ctr = 0;
   __syncthreads();
@@ -479,6 +480,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
   const bool folder = hl == 0;
   const int nsub = bs >> 4;
   if (lane < 16) S.zero[lane] = 0;
+  // launched programmatically dependent on the order kernel (when there is
+  // one): wait for its order / counter before reading anything
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   Cursor P[V];
 #pragma unroll
@@ -692,8 +696,24 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
     } else {
       KVX_CUDA(cudaMemsetAsync(ws + 1, 0, sizeof(unsigned long long), s));
     }
-    hw::halfwarp_hash_kernel<1><<<sm_count(dev), warps * 32, smem, s>>>(
-        d_tokens, d_tok_off, n_req, static_cast<int>(bs), d_key_off, d_keys, order, ws + 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sm_count(dev));
+    cfg.blockDim = dim3(warps * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    static const bool pdl = [] {
+      const char* e = std::getenv("KVX_HASH_PDL");
+      return !(e && e[0] == '0');
+    }();
+    cfg.numAttrs = (order && pdl) ? 1 : 0;  // PDL only behind our own order kernel
+    const int bsi = static_cast<int>(bs);
+    unsigned long long* ctr = ws + 1;
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, hw::halfwarp_hash_kernel<1>, d_tokens, d_tok_off, n_req,
+                                bsi, d_key_off, d_keys, static_cast<const int32_t*>(order), ctr));
     KVX_LAUNCH_CHECK("halfwarp_hash_kernel");
     return KVX_OK;
   }
