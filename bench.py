@@ -602,7 +602,10 @@ def run_kvx(args):
                        "pairs": role.pairs,
                        "parallelism": ("local (prefill+decode on one GPU)" if world == 1 else
                                        f"{role.pairs}P->{role.pairs}D pairs"),
-                       "l2": "inputs far larger than L2 (126 MB); no flush needed"},
+                       "l2": ("inputs far larger than L2 (126 MB); no flush needed" +
+                              ("; inside one layer launch the wave's requests re-read the shared "
+                               "prefix slabs of that layer, which then hit L2 (part of the "
+                               "workload's 50% prefix sharing)" if args.config == 2 else ""))},
             "roofline": roof,
             "link": (None if world == 1 else {
                 "achieved_per_pair": value / role.pairs, "peak_per_direction": link_gbs,
