@@ -361,9 +361,10 @@ int launch_tma(const SlabCopy& c, int dev, int ctas_per_sm, cudaStream_t s) {
   return KVX_OK;
 }
 
-thread_local bool t_overlap_prev = false;  // set by copy_paged_overlapped
-
-int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
+// overlap_prev: launch with programmatic stream serialization (the copy may
+// start while the previous kernel on the stream runs; caller guarantees the
+// two touch disjoint bytes).  LSU copy only.
+int launch_copy(const SlabCopy& c, int dev, cudaStream_t s, bool overlap_prev = false) {
   const int64_t units = c.planes * c.n;
   if (units == 0 || c.slab == 0) return KVX_OK;
   const int sms = sm_count(dev);
@@ -398,7 +399,7 @@ int launch_copy(const SlabCopy& c, int dev, cudaStream_t s) {
     }();
     if (variant == 1) {
       copy_lsu_plain_kernel<<<blocks, kLsuThreads, 0, s>>>(c);
-    } else if (t_overlap_prev) {
+    } else if (overlap_prev) {
       // programmatic dependent launch: this copy may start while the previous
       // kernel on the stream is still running (caller guarantees independence)
       cudaLaunchConfig_t cfg = {};
@@ -513,6 +514,36 @@ int check_range(const kvx_pool* p, int64_t n, int32_t lo, int32_t hi) {
 }
 
 }  // namespace
+
+namespace kvx {
+namespace {
+// Checks and the SlabCopy of a paged -> paged copy of blocks [0, n), layers [lo, hi).
+int paged_copy_args(const kvx_pool* src, const int32_t* d_src_table, const kvx_pool* dst,
+                    const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, SlabCopy* c,
+                    bool* empty) {
+  int st = check_range(src, n, lo, hi);
+  if (st) return st;
+  st = check_range(dst, n, lo, hi);
+  if (st) return st;
+  KVX_REQUIRE(src->slab == dst->slab, "kvx_copy_paged: slab sizes differ");
+  *empty = n == 0 || lo == hi;
+  if (*empty) return KVX_OK;
+  KVX_REQUIRE(d_src_table && d_dst_table, "kvx_copy_paged: NULL table");
+  c->src = src->base + static_cast<int64_t>(lo) * 2 * src->d.slots * src->slab;
+  c->src_plane = src->d.slots * src->slab;
+  c->src_table = d_src_table;
+  c->dst = dst->base + static_cast<int64_t>(lo) * 2 * dst->d.slots * dst->slab;
+  c->dst_plane = dst->d.slots * dst->slab;
+  c->dst_table = d_dst_table;
+  c->n = n;
+  c->src_slots = static_cast<uint32_t>(src->d.slots);
+  c->dst_slots = static_cast<uint32_t>(dst->d.slots);
+  c->planes = static_cast<int64_t>(hi - lo) * 2;
+  c->slab = src->slab;
+  return KVX_OK;
+}
+}  // namespace
+}  // namespace kvx
 
 extern "C" {
 
@@ -651,25 +682,10 @@ int kvx_scatter(kvx_pool* p, const int32_t* d_dst_table, int64_t n, int32_t lo, 
 
 int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
                    const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, void* stream) {
-  int st = check_range(src, n, lo, hi);
-  if (st) return st;
-  st = check_range(dst, n, lo, hi);
-  if (st) return st;
-  KVX_REQUIRE(src->slab == dst->slab, "kvx_copy_paged: slab sizes differ");
-  if (n == 0 || lo == hi) return KVX_OK;
-  KVX_REQUIRE(d_src_table && d_dst_table, "kvx_copy_paged: NULL table");
   SlabCopy c;
-  c.src = src->base + static_cast<int64_t>(lo) * 2 * src->d.slots * src->slab;
-  c.src_plane = src->d.slots * src->slab;
-  c.src_table = d_src_table;
-  c.dst = dst->base + static_cast<int64_t>(lo) * 2 * dst->d.slots * dst->slab;
-  c.dst_plane = dst->d.slots * dst->slab;
-  c.dst_table = d_dst_table;
-  c.n = n;
-  c.src_slots = static_cast<uint32_t>(src->d.slots);
-  c.dst_slots = static_cast<uint32_t>(dst->d.slots);
-  c.planes = static_cast<int64_t>(hi - lo) * 2;
-  c.slab = src->slab;
+  bool empty = false;
+  const int st = kvx::paged_copy_args(src, d_src_table, dst, d_dst_table, n, lo, hi, &c, &empty);
+  if (st || empty) return st;
   DeviceGuard g(src->d.device);
   return launch_copy(c, src->d.device, as_stream(stream));
 }
@@ -680,25 +696,11 @@ namespace kvx {
 int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
                     const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, void* stream,
                     const uint64_t* d_flag, uint64_t value, bool overlap_prev) {
-  int st = check_range(src, n, lo, hi);
-  if (st) return st;
-  st = check_range(dst, n, lo, hi);
-  if (st) return st;
-  KVX_REQUIRE(src->slab == dst->slab, "copy_paged_pull: slab sizes differ");
-  if (n == 0 || lo == hi) return KVX_OK;
-  KVX_REQUIRE(d_src_table && d_dst_table && d_flag, "copy_paged_pull: NULL argument");
   SlabCopy c;
-  c.src = src->base + static_cast<int64_t>(lo) * 2 * src->d.slots * src->slab;
-  c.src_plane = src->d.slots * src->slab;
-  c.src_table = d_src_table;
-  c.dst = dst->base + static_cast<int64_t>(lo) * 2 * dst->d.slots * dst->slab;
-  c.dst_plane = dst->d.slots * dst->slab;
-  c.dst_table = d_dst_table;
-  c.n = n;
-  c.src_slots = static_cast<uint32_t>(src->d.slots);
-  c.dst_slots = static_cast<uint32_t>(dst->d.slots);
-  c.planes = static_cast<int64_t>(hi - lo) * 2;
-  c.slab = src->slab;
+  bool empty = false;
+  const int st = paged_copy_args(src, d_src_table, dst, d_dst_table, n, lo, hi, &c, &empty);
+  if (st || empty) return st;
+  KVX_REQUIRE(d_flag, "copy_paged_pull: NULL flag");
   const int dev = dst->d.device;  // the pulling GPU
   DeviceGuard g(dev);
   const int64_t items = c.planes * c.n * ((c.slab + kLsuItem - 1) / kLsuItem);
@@ -725,10 +727,12 @@ int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* d
 int copy_paged_overlapped(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
                           const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi,
                           void* stream) {
-  t_overlap_prev = true;
-  const int rc = kvx_copy_paged(src, d_src_table, dst, d_dst_table, n, lo, hi, stream);
-  t_overlap_prev = false;
-  return rc;
+  SlabCopy c;
+  bool empty = false;
+  const int st = paged_copy_args(src, d_src_table, dst, d_dst_table, n, lo, hi, &c, &empty);
+  if (st || empty) return st;
+  DeviceGuard g(src->d.device);
+  return launch_copy(c, src->d.device, as_stream(stream), true);
 }
 }  // namespace kvx
 
