@@ -337,7 +337,9 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
           // call waits for everything before it (an earlier send may have
           // written the same decode slots), and a launch sampled for timing
           // runs isolated so its duration is its own.
-          const bool overlap = pdl_enabled() && !first_unit && !will_sample(s);
+          // (a pool copied into itself keeps its units strictly ordered)
+          const bool overlap =
+              pdl_enabled() && !first_unit && !will_sample(s) && s->src != s->dst;
           rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
             return overlap ? kvx::copy_paged_overlapped(s->src, d_src_table + b0, s->dst,
                                                         d_dst_table + b0, nb, l0, l1, s->s_main)
