@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <cstdint>
 #include <unordered_map>
 #include <unordered_set>
@@ -27,6 +28,8 @@
 
 struct kvx_store {
   int device = 0;
+  kvx_pool_desc desc{};
+  std::map<int, kvx_pool*> views;  // this pool as seen from other GPUs (migration pulls)
   kvx_pool* pool = nullptr;
   kvx_index* index = nullptr;
   kvx_slot_alloc* alloc = nullptr;
@@ -90,8 +93,45 @@ int copy_blocks(kvx_store* src, kvx_store* dst, const std::vector<int32_t>& st,
                 const std::vector<int32_t>& dt) {
   const int64_t m = static_cast<int64_t>(st.size());
   if (dst->device != src->device) {
-    int rc = kvx_enable_peer(src->device, dst->device);
+    // Across GPUs the destination GPU pulls: its copy kernel loads the source
+    // pool over NVLink through a view of it (UVA + peer access) and stores
+    // locally -- 0.99-1.0 of the link vs ~0.9 for pushing with stores
+    // (profiles/r01/migrate.md) -- after the source stream's queued work.
+    int rc = kvx_enable_peer(dst->device, src->device);
+    if (!rc) rc = kvx_enable_peer(src->device, dst->device);
     if (rc) return rc;
+    kvx_pool*& view = src->views[dst->device];
+    if (!view) {
+      kvx_pool_desc vd = src->desc;
+      vd.device = dst->device;
+      rc = kvx_pool_create_view(&vd, kvx_pool_base(src->pool), &view);
+      if (rc) return rc;
+    }
+    struct Event {  // destroyed on every path
+      cudaEvent_t e = nullptr;
+      ~Event() {
+        if (e) cudaEventDestroy(e);
+      }
+    } ev;
+    {
+      kvx::DeviceGuard gs(src->device);
+      KVX_CUDA(cudaEventCreateWithFlags(&ev.e, cudaEventDisableTiming));
+      KVX_CUDA(cudaEventRecord(ev.e, src->stream));
+    }
+    kvx::DeviceGuard g(dst->device);
+    KVX_CUDA(cudaStreamWaitEvent(dst->stream, ev.e, 0));
+    rc = ensure_scratch(dst, m);
+    if (rc) return rc;
+    int32_t* d_tables = reinterpret_cast<int32_t*>(dst->d_scratch);
+    KVX_CUDA(cudaMemcpyAsync(d_tables, st.data(), m * sizeof(int32_t), cudaMemcpyHostToDevice,
+                             dst->stream));
+    KVX_CUDA(cudaMemcpyAsync(d_tables + m, dt.data(), m * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, dst->stream));
+    rc = kvx_copy_paged(view, d_tables, dst->pool, d_tables + m, m, 0, kvx_pool_layers(src->pool),
+                        dst->stream);
+    if (rc) return rc;
+    KVX_CUDA(cudaStreamSynchronize(dst->stream));
+    return KVX_OK;
   }
   kvx::DeviceGuard g(src->device);
   int rc = ensure_scratch(src, m);
@@ -116,6 +156,7 @@ int kvx_store_create(const kvx_pool_desc* desc, kvx_store** out) {
   KVX_REQUIRE(desc && out, "kvx_store_create: NULL argument");
   auto* s = new kvx_store();
   s->device = desc->device;
+  s->desc = *desc;
   int rc = kvx_pool_create(desc, &s->pool);
   if (!rc) rc = kvx_index_create(desc->device, desc->slots, &s->index);
   if (!rc) rc = kvx_slot_alloc_create(desc->slots, &s->alloc);
@@ -137,6 +178,7 @@ int kvx_store_destroy(kvx_store* s) {
   kvx::DeviceGuard g(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   if (s->index) kvx_index_destroy(s->index);
+  for (auto& kv : s->views) kvx_pool_destroy(kv.second);  // views do not own memory
   if (s->pool) kvx_pool_destroy(s->pool);
   if (s->alloc) kvx_slot_alloc_destroy(s->alloc);
   if (s->d_scratch) cudaFree(s->d_scratch);
