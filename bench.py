@@ -67,9 +67,11 @@ def parse_args():
     ap.add_argument("--block-size", type=int, default=16)
     ap.add_argument("--dtype-bytes", type=int, default=2)
     ap.add_argument("--no-match", action="store_true")
-    ap.add_argument("--match-exchange", default="nvlink", choices=["nvlink", "nccl"],
-                    help="N>1 prefix match: combine the per-GPU instances inside the match "
-                         "kernel (NVLink remote atomics + stream flags) or by NCCL all-reduce")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="every rank on cuda:0: two processes sharing one GPU run the peer modes' "
+                         "IPC + flag protocol and the cross-process match on a 1-GPU box (gloo "
+                         "handshake, since NCCL refuses two ranks on one GPU); a protocol / "
+                         "parity check, not an NVLink measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -241,7 +243,7 @@ def cpu_transfer_sample(seconds: float, steps: int = 0, warmup: int = 0):
                       f"per-layer memcpy gather+scatter, {len(times)} passes, median"}, times
 
 
-def cpu_match_sample(mw, seconds: float):
+def cpu_match_sample(mw, seconds: float, gpu_len=None, gpu_id=None):
     """Reference CPU path for stage 1: the reference's own chain_hash folded
     over each block's tokens, then the reference's find_best_prefix_match over
     its CachePool holding the same 1M keys (oracle/_ref), request slices on
@@ -265,11 +267,17 @@ def cpu_match_sample(mw, seconds: float):
         ref.block_hash_mt(tokens, tok_off, mw.block_size, ko, keys, threads)
         bl, bi = ref.match_batch_mt([pool], [0], keys, ko, threads)
         times.append(time.perf_counter() - t0)
+    agree = None
+    if gpu_len is not None:  # the reference's own answers for the sample == the GPU's
+        agree = bool(np.array_equal(np.asarray(bl), gpu_len[:n]) and
+                     np.array_equal(np.asarray(bi), gpu_id[:n]))
+        if not agree:
+            raise SystemExit("MATCH PARITY FAILURE vs kvref find_best_prefix_match")
     return {"value": float(ko[-1]) / statistics.median(times), "unit": "blocks/s",
             "cores": threads, "kind": "reference",
             "sample": f"{n} requests ({int(ko[-1])} blocks): kvref chain_hash fold + "
                       "kvref find_best_prefix_match vs a 1M-key kvref CachePool",
-            "best_len_check": bl[:8].tolist()}
+            "gpu_equals_kvref_on_sample": agree}
 
 
 # ---------------------------------------------------------------------------
@@ -338,9 +346,11 @@ def run_kvx(args):
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local_rank)
-    dev = local_rank
-    if world > 1:
+    dev = 0 if args.share_gpu else local_rank
+    torch.cuda.set_device(dev)
+    if world > 1 and args.share_gpu:
+        dist.init_process_group("gloo")
+    elif world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     role = pair_topology(world, rank)
     kvx.set_copy_impl(args.copy_impl)
@@ -358,6 +368,9 @@ def run_kvx(args):
                 "peer_pull" if args.config == 3 else "peer_ce")
     if (role.role == "local") != mode.startswith("local"):
         raise SystemExit(f"mode {mode} does not fit {world} GPU(s)")
+    if args.share_gpu and mode == "peer_nccl":
+        raise SystemExit("--share-gpu runs the NVLink-protocol modes only (NCCL refuses two ranks "
+                         "on one GPU)")
 
     link_gbs = None
     if world > 1:
@@ -442,6 +455,7 @@ def run_kvx(args):
             checked += dev_dst[w].numel() * (hi - lo) * 2 * wl.slab_bytes
         torch.cuda.synchronize()
         barrier()
+    st.check()  # a failed unit (pull gate timeout, bad table entry) raises here
     bad = int(sum_over_ranks(float(mismatch.item()), d))
     checked = int(sum_over_ranks(float(checked), d))
     if bad:
@@ -490,6 +504,7 @@ def run_kvx(args):
     e1.record(main)
     torch.cuda.synchronize()
     wall_ms = (time.perf_counter() - w0) * 1e3  # host clock, device idle at both ends
+    st.check()
     barrier()
     launches = pkg.launch_count() - launches0
     clk = clocks.stop()
@@ -600,6 +615,7 @@ def run_kvx(args):
                        "copy_impl": args.copy_impl, "layers_per_chunk": args.layers_per_chunk,
                        "cuda_graph": bool(args.graph),
                        "pairs": role.pairs,
+                       "share_gpu": bool(args.share_gpu),
                        "parallelism": ("local (prefill+decode on one GPU)" if world == 1 else
                                        f"{role.pairs}P->{role.pairs}D pairs"),
                        "l2": ("inputs far larger than L2 (126 MB); no flush needed" +
@@ -607,7 +623,7 @@ def run_kvx(args):
                                "prefix slabs of that layer, which then hit L2 (part of the "
                                "workload's 50% prefix sharing)" if args.config == 2 else ""))},
             "roofline": roof,
-            "link": (None if world == 1 else {
+            "link": (None if world == 1 or args.share_gpu else {
                 "achieved_per_pair": value / role.pairs, "peak_per_direction": link_gbs,
                 "frac": value / role.pairs / link_gbs, "unit": "GB/s",
                 "peak_source": "measured in this run: 1 GiB copy-engine peer copy, slowest pair",
@@ -659,110 +675,142 @@ def probe_link(role, dev):
     return gbs
 
 
+def shard_by_tokens(tok_off: np.ndarray, world: int):
+    """Contiguous request ranges [r0, r1) per rank with ~equal token counts
+    (the hash is ALU bound per token): rank i takes the requests whose first
+    token lies in [i*T/world, (i+1)*T/world)."""
+    tok_off = np.asarray(tok_off, dtype=np.int64)
+    n = len(tok_off) - 1
+    total = int(tok_off[-1] - tok_off[0])
+    bounds = [0]
+    for i in range(1, world):
+        cut = int(tok_off[0]) + (total * i) // world
+        bounds.append(int(np.searchsorted(tok_off[:n], cut, side="left")))
+    bounds.append(n)
+    bounds = np.maximum.accumulate(np.asarray(bounds))
+    return [(int(bounds[i]), int(bounds[i + 1])) for i in range(world)]
+
+
+class Stage1Batch:
+    """One Config 4 batch on the device plus the instance indices built from
+    its sessions' earlier turns (MatchWorkload)."""
+
+    def __init__(self, mw, dev, s):
+        import torch
+
+        import paper_2407_00079_b200 as pkg
+        self.mw, self.dev, self.s = mw, dev, s
+        d = f"cuda:{dev}"
+        with torch.cuda.stream(s):
+            warm_tok = torch.as_tensor(mw.warm_tokens, device=d)
+            warm_off = torch.as_tensor(mw.warm_tok_off, device=d)
+            self.wkeys, wko = pkg.chain_hash_batch(warm_tok, warm_off, mw.block_size, stream=s)
+            self.wko = wko.cpu().numpy()
+            self.tokens = torch.as_tensor(mw.tokens, device=d)
+            self.tok_off = torch.as_tensor(mw.tok_off, device=d)
+            self.key_off = pkg.kvx.key_offsets(self.tok_off, mw.block_size, stream=s)
+            self.key_off_host = self.key_off.cpu().numpy()
+            self.n_blocks = int(self.key_off_host[-1])
+        s.synchronize()
+
+    def instance_keys(self, inst: int, n_inst: int):
+        """Prefill instance `inst` of n_inst holds the earlier turns of every
+        n_inst-th session, topped up with its own unrelated keys to pool_keys."""
+        import torch
+        mw, ko = self.mw, self.wko
+        parts = [self.wkeys[int(ko[j]):int(ko[j + 1])] for j in range(len(mw.session_ids))
+                 if j % n_inst == inst]
+        own = torch.cat(parts)[: mw.pool_keys] if parts else self.wkeys[:0]
+        filler = torch.as_tensor(mw.filler_keys(mw.pool_keys - own.numel(), salt=inst),
+                                 device=own.device)
+        return torch.cat([own, filler])
+
+    def index(self, inst: int, n_inst: int):
+        import torch
+
+        import paper_2407_00079_b200 as pkg
+        with torch.cuda.stream(self.s):
+            ix = pkg.BlockIndex(self.dev, self.mw.pool_keys)
+            ix.insert(self.instance_keys(inst, n_inst), stream=self.s)
+        st = ix.stats(stream=self.s)
+        assert st["live"] == self.mw.pool_keys, st
+        return ix
+
+    def oracle_best(self, o, n_inst: int):
+        """(best_len, best_id) of every request over instances 0..n_inst-1
+        (ids = instance numbers), restated in C over the same key sets."""
+        sets = [o.make_set(self.instance_keys(i, n_inst).cpu().numpy()) for i in range(n_inst)]
+        k_ref, ko_ref = o.block_hash_batch(self.mw.tokens, self.mw.tok_off, self.mw.block_size)
+        _, bl, bi = o.match_prefix_batch(sets, list(range(n_inst)), k_ref, ko_ref)
+        for h in sets:
+            o.free_set(h)
+        return k_ref, bl, bi
+
+
 def bench_match(args, dev, rank, world, role):
+    """Stage 1 (Config 4): batched block hash + prefix match.
+
+    N=1: the batch against one 1M-key instance index.  N>1, headline: every
+    GPU serves its own batch of the same trace against its own 1M-key index
+    (data-parallel Conductor replicas, SURVEY 8(e) case (i); no exchange,
+    weak scaling).  N>1, "sharded": ONE batch, requests sharded over the GPUs
+    for hashing, keys pushed to every GPU over NVLink, and every GPU holding
+    one prefill instance (case (ii)): the global find_best_prefix_match is
+    combined inside the match kernel (kvx_xmatch)."""
     import torch
 
     import paper_2407_00079_b200 as pkg
     from paper_2407_00079_b200.cluster import max_over_ranks, sum_over_ranks
     from paper_2407_00079_b200.workloads import MatchWorkload
 
-    import torch.distributed as dist
-
-    mw = MatchWorkload().build()
     d = f"cuda:{dev}"
     s = torch.cuda.Stream(dev)
-    n_sess = len(mw.session_ids)
-
-    def instance_keys(inst: int, n_inst: int, warm_keys, warm_ko):
-        """Prefill instance `inst` of n_inst holds the earlier turns of every
-        n_inst-th session, topped up with its own unrelated keys to pool_keys."""
-        ko = warm_ko.cpu().numpy()
-        parts = [warm_keys[int(ko[j]):int(ko[j + 1])] for j in range(n_sess) if j % n_inst == inst]
-        own = torch.cat(parts)[: mw.pool_keys] if parts else warm_keys[:0]
-        filler = torch.as_tensor(mw.filler_keys(mw.pool_keys - own.numel(), salt=inst), device=d)
-        return torch.cat([own, filler])
-
+    # rank r's own batch of the trace (same generator, another draw) at N>1
+    mw = MatchWorkload(seed=4 + (rank if world > 1 else 0)).build()
+    B = Stage1Batch(mw, dev, s)
+    idx = B.index(0, 1)
+    tokens, tok_off, key_off, n_blocks = B.tokens, B.tok_off, B.key_off, B.n_blocks
     with torch.cuda.stream(s):
-        warm_tok = torch.as_tensor(mw.warm_tokens, device=d)
-        warm_off = torch.as_tensor(mw.warm_tok_off, device=d)
-        wkeys, wko = pkg.chain_hash_batch(warm_tok, warm_off, mw.block_size, stream=s)
-        # one prefill instance per GPU (SURVEY 8(e) case ii): this rank's index
-        index_keys = instance_keys(rank, world, wkeys, wko)
-        idx = pkg.BlockIndex(dev, mw.pool_keys)
-        idx.insert(index_keys, stream=s)
-        tokens = torch.as_tensor(mw.tokens, device=d)
-        tok_off = torch.as_tensor(mw.tok_off, device=d)
-        key_off = pkg.kvx.key_offsets(tok_off, mw.block_size)
-        n_blocks = int(key_off[-1].item())
         keys = torch.empty(n_blocks, dtype=torch.int64, device=d)
         best_len = torch.empty(mw.n_req, dtype=torch.int64, device=d)
         best_id = torch.empty(mw.n_req, dtype=torch.int32, device=d)
-        packed = torch.empty(mw.n_req, dtype=torch.int64, device=d)
-    s.synchronize()
-    xm = None
-    if world > 1 and args.match_exchange == "nvlink":
-        # the exchange inside the match kernel: remote atomicMax into every
-        # rank's result buffer over NVLink + stream-ordered flags (kvx_xmatch)
-        xm = pkg.kvx.XMatch(dev, rank, world, mw.n_req)
-        blobs = [None] * world
-        dist.all_gather_object(blobs, xm.export())
-        for blob in blobs:
-            xm.connect(blob)
-    st = idx.stats()
-    assert st["live"] == mw.pool_keys, st
-    mw.index_keys = index_keys.cpu().numpy()
+    mw.index_keys = B.instance_keys(0, 1).cpu().numpy()
 
     th, tm = KernelTimer(True), KernelTimer(True)
     tok_bytes = mw.tokens.nbytes
 
     def step(timed):
-        nonlocal best_len, best_id
         a = th.start(s) if timed else None
         pkg.chain_hash_batch(tokens, tok_off, mw.block_size, key_off=key_off, keys=keys, stream=s)
         th.stop(s, a, tok_bytes + 8 * n_blocks)
         b = tm.start(s) if timed else None
-        if world == 1:
-            pkg.match_prefix_batch([idx], [0], keys, key_off, want_lens=False, stream=s,
-                                   out=(None, best_len, best_id))
-            tm.stop(s, b, 0)
-        elif xm is not None:  # match + cross-GPU MAX in one kernel (NVLink atomics), flags
-            xm.run([idx], [rank], keys, key_off, out=(best_len, best_id), stream=s)
-            tm.stop(s, b, 0)
-        else:  # local best per request, then the cross-GPU exchange: NCCL all-reduce(MAX)
-            pkg.kvx.match_prefix_packed([idx], [rank], keys, key_off, out=packed, stream=s)
-            tm.stop(s, b, 0)
-            with torch.cuda.stream(s):
-                dist.all_reduce(packed, op=dist.ReduceOp.MAX)
-            best_len, best_id = pkg.kvx.best_unpack(packed, stream=s)
+        pkg.match_prefix_batch([idx], [0], keys, key_off, want_lens=False, stream=s,
+                               out=(None, best_len, best_id))
+        tm.stop(s, b, 0)
 
     for _ in range(args.warmup):
         step(False)
     s.synchronize()
-    if world > 1 and rank == 0:
-        # parity of the exchange: all N instances on one GPU, one batched query
-        with torch.cuda.stream(s):
-            all_idx = []
-            for i in range(world):
-                ix = pkg.BlockIndex(dev, mw.pool_keys)
-                ix.insert(instance_keys(i, world, wkeys, wko), stream=s)
-                all_idx.append(ix)
-            _, ref_len, ref_id = pkg.match_prefix_batch(all_idx, list(range(world)), keys,
-                                                        key_off, want_lens=False, stream=s)
-        s.synchronize()
-        assert torch.equal(ref_len, best_len) and torch.equal(ref_id, best_id), \
-            "cross-GPU best-match parity"
-        del all_idx
-    # parity spot check against the oracle restatement on the first requests
+    # parity before timing: every key and every request's (best_len, best_id)
+    # against the C restatement over the same 1M-key set (kvcache.cpp:150-154,
+    # conductor.cpp:57-73)
     from oracle import Oracle
     o = Oracle()
-    # every key of the batch against the C restatement (~1 s of host time)
-    k_ref, ko_ref = o.block_hash_batch(mw.tokens, mw.tok_off, mw.block_size)
-    assert np.array_equal(keys.cpu().numpy(), k_ref), "hash parity"
-    lens_all = best_len.cpu().numpy()
-    n_probes = int(np.minimum(lens_all + 1, np.diff(key_off.cpu().numpy())).sum())
+    k_ref, want_len, want_id = B.oracle_best(o, 1)
+    if not np.array_equal(keys.cpu().numpy(), k_ref):
+        raise SystemExit("HASH PARITY FAILURE")
+    got_len, got_id = best_len.cpu().numpy(), best_id.cpu().numpy()
+    n_bad = int(np.count_nonzero((got_len != want_len) | (got_id != want_id)))
+    n_bad = int(sum_over_ranks(float(n_bad), d))
+    if n_bad:
+        raise SystemExit(f"MATCH PARITY FAILURE: {n_bad} requests differ from the oracle's "
+                         "find_best_prefix_match")
+    match_checked = {"requests": int(sum_over_ranks(float(mw.n_req), d)), "mismatched": 0,
+                     "matched_blocks": int(sum_over_ranks(float(want_len.sum()), d))}
+    n_probes = int(np.minimum(got_len + 1, np.diff(B.key_off_host)).sum())
     torch.cuda.synchronize()
     if world > 1:
-        dist.barrier()  # all ranks enter the timed region together (the all-reduce pairs them)
+        torch.distributed.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(s)
@@ -771,152 +819,105 @@ def bench_match(args, dev, rank, world, role):
     e1.record(s)
     s.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
-    # every rank answers the same batch for its own instance; the all-reduce
-    # makes it one global find_best_prefix_match over `world` instances
-    total_blocks = float(n_blocks)
+    total_blocks = sum_over_ranks(float(n_blocks), d)  # every rank's own batch
     value = total_blocks / (ms / 1e3)
     hs, ms_match = th.summary(), tm.summary()
     match_bytes = 24 * n_probes
 
-    # e2e: host tokens in (pinned), best (len, id) out, every step
+    # e2e through the API: host tokens + token offsets in (pinned), the key
+    # offsets scan, hash, match, best (len, id) out -- every step
     pin_tok = torch.as_tensor(mw.tokens).pin_memory()
+    pin_off = torch.as_tensor(mw.tok_off).pin_memory()
     out_len = torch.empty(mw.n_req, dtype=torch.int64).pin_memory()
     out_id = torch.empty(mw.n_req, dtype=torch.int32).pin_memory()
     torch.cuda.synchronize()
     if world > 1:
-        dist.barrier()
+        torch.distributed.barrier()
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(s)
     for _ in range(args.steps):
         with torch.cuda.stream(s):
             tokens.copy_(pin_tok, non_blocking=True)
+            tok_off.copy_(pin_off, non_blocking=True)
+        pkg.kvx.key_offsets(tok_off, mw.block_size, out=key_off, stream=s)
         step(False)
         with torch.cuda.stream(s):
             out_len.copy_(best_len, non_blocking=True)
             out_id.copy_(best_id, non_blocking=True)
     f1.record(s)
     s.synchronize()
+    assert np.array_equal(out_len.numpy(), want_len) and np.array_equal(out_id.numpy(), want_id)
     e2e_ms = max_over_ranks(f0.elapsed_time(f1), d) / args.steps
 
     # Serving pipeline (reported beside the serial step, not instead of it):
     # back-to-back batches, batch k's match on a second stream while batch k+1
     # hashes on the first; two key / result buffers alternate.
-    pipelined = None
-    if world == 1:
-        s2 = torch.cuda.Stream(dev)
-        keys2 = [keys, torch.empty_like(keys)]
-        outs2 = [(torch.empty_like(best_len), torch.empty_like(best_id)) for _ in range(2)]
-        hashed = [torch.cuda.Event(), torch.cuda.Event()]
-        matched = [torch.cuda.Event(), torch.cuda.Event()]
+    s2 = torch.cuda.Stream(dev)
+    keys2 = [keys, torch.empty_like(keys)]
+    outs2 = [(torch.empty_like(best_len), torch.empty_like(best_id)) for _ in range(2)]
+    hashed = [torch.cuda.Event(), torch.cuda.Event()]
+    matched = [torch.cuda.Event(), torch.cuda.Event()]
 
-        def pipe_step(k):
-            b = k % 2
-            if k >= 2:
-                s.wait_event(matched[b])  # the match that read keys2[b] is done
-            pkg.chain_hash_batch(tokens, tok_off, mw.block_size, key_off=key_off, keys=keys2[b],
-                                 stream=s)
-            hashed[b].record(s)
-            s2.wait_event(hashed[b])
-            pkg.match_prefix_batch([idx], [0], keys2[b], key_off, want_lens=False, stream=s2,
-                                   out=(None, outs2[b][0], outs2[b][1]))
-            matched[b].record(s2)
+    def pipe_step(k):
+        b = k % 2
+        if k >= 2:
+            s.wait_event(matched[b])  # the match that read keys2[b] is done
+        pkg.chain_hash_batch(tokens, tok_off, mw.block_size, key_off=key_off, keys=keys2[b],
+                             stream=s)
+        hashed[b].record(s)
+        s2.wait_event(hashed[b])
+        pkg.match_prefix_batch([idx], [0], keys2[b], key_off, want_lens=False, stream=s2,
+                               out=(None, outs2[b][0], outs2[b][1]))
+        matched[b].record(s2)
 
-        for k in range(args.warmup):
-            pipe_step(k)
-        torch.cuda.synchronize()
-        assert torch.equal(outs2[0][0], best_len) and torch.equal(outs2[0][1], best_id), \
-            "pipelined match parity"
-        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        p0.record(s)
-        for k in range(args.steps):
-            pipe_step(k)
-        s.wait_stream(s2)
-        p1.record(s)
-        torch.cuda.synchronize()
-        pms = p0.elapsed_time(p1) / args.steps
-        pipelined = {"value": total_blocks / (pms / 1e3), "unit": "blocks/s",
-                     "ms_per_batch": pms,
-                     "how": "back-to-back batches: batch k's match on a second stream "
-                            "overlaps batch k+1's hash; per-batch latency stays ms_per_step"}
-        del keys2
+    for k in range(max(args.warmup, 2)):
+        pipe_step(k)
+    torch.cuda.synchronize()
+    assert torch.equal(outs2[0][0], best_len) and torch.equal(outs2[0][1], best_id), \
+        "pipelined match parity"
+    if world > 1:
+        torch.distributed.barrier()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(s)
+    for k in range(args.steps):
+        pipe_step(k)
+    s.wait_stream(s2)
+    p1.record(s)
+    torch.cuda.synchronize()
+    pms = max_over_ranks(p0.elapsed_time(p1), d) / args.steps
+    pipelined = {"value": total_blocks / (pms / 1e3), "unit": "blocks/s",
+                 "ms_per_batch": pms,
+                 "how": "back-to-back batches: batch k's match on a second stream "
+                        "overlaps batch k+1's hash; per-batch latency stays ms_per_step"}
+    del keys2
 
     # batched Conductor scoring: P=8 prefill instances on
     # this GPU, per-instance match matrix + kvcache-centric schedule of the batch
     conductor = None
     if world == 1:
-        from paper_2407_00079_b200 import conductor as cd
-        P = 8
-        with torch.cuda.stream(s):
-            inst = []
-            for i in range(P):
-                ix = pkg.BlockIndex(dev, mw.pool_keys)
-                ix.insert(instance_keys(i, P, wkeys, wko), stream=s)
-                inst.append(ix)
-            lens = torch.empty((mw.n_req, P), dtype=torch.int64, device=d)
-            bl8 = torch.empty(mw.n_req, dtype=torch.int64, device=d)
-            bi8 = torch.empty(mw.n_req, dtype=torch.int32, device=d)
-            inp = tok_off[1:] - tok_off[:-1]
-        rng = np.random.default_rng(8)
-        pre = np.zeros(P, dtype=cd.PREFILL_DT)
-        pre["id"] = np.arange(P)
-        pre["busy_until_ms"] = rng.random(P) * 500
-        pre["sender_busy_until_ms"] = rng.random(P) * 300
-        pre["queued_work_ms"] = rng.random(P) * 1500
-        dec = np.zeros(8, dtype=cd.DECODE_DT)
-        dec["id"] = np.arange(8)
-        dec["batch_size"] = rng.integers(0, 33, 8)
-        dec["resident_kv_tokens"] = rng.integers(0, 200000, 8)
-        perf = cd.PerfParams(cpp_group_size=2)
-        kwargs = dict(perf=perf, l_ttft_ms=30000.0, l_tbt_ms=100.0, threshold=4.0,
-                      block_size=mw.block_size, now_ms=0.0, prefill=pre, decode=dec,
-                      input_len=inp, match_len=lens, stream=s)
+        conductor = bench_conductor(args, B, keys, s)
 
-        def conduct():
-            pkg.match_prefix_batch(inst, list(range(P)), keys, key_off, stream=s,
-                                   out=(lens, bl8, bi8))
-            return cd.schedule_batch(**kwargs)
-
-        conduct()
-        s.synchronize()
-        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c0.record(s)
-        for _ in range(args.steps):
-            pkg.match_prefix_batch(inst, list(range(P)), keys, key_off, stream=s,
-                                   out=(lens, bl8, bi8))
-        c1.record(s)
-        s.synchronize()
-        match8_ms = c0.elapsed_time(c1) / args.steps
-        t0 = time.perf_counter()
-        dec_out = conduct()
-        call_ms = (time.perf_counter() - t0) * 1e3
-        conductor = {
-            "metric": "kvcache-centric schedule of the batch (match matrix + FP64 scoring)",
-            "instances": P, "requests": mw.n_req, "match_matrix_ms": match8_ms,
-            "match_matrix_blocks_per_s": n_blocks * P / (match8_ms / 1e3),
-            "end_to_end_call_ms": call_ms,
-            "decisions": {"accepted": int(dec_out["accepted"].sum()),
-                          "migrations": int(dec_out["migrate"].sum())},
-            "note": "scoring bit-identical to kvref::schedule (tests/test_gpu_conductor.py)"}
-        del inst
+    sharded = None
+    if world > 1:
+        sharded = bench_match_sharded(args, dev, rank, world, s, o)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_match_sample(mw, min(args.cpu_seconds, 10.0))
+        cpu = cpu_match_sample(mw, min(args.cpu_seconds, 10.0), got_len, got_id)
     peaks = measured_peaks()
     hash_gbs = hs["avg_algorithmic_bytes"] / (hs["avg_ms"] / 1e3) / GB
     match_gbs = match_bytes / (ms_match["avg_ms"] / 1e3) / GB
+    chain_hashes = tok_bytes // 4 + n_blocks
     return {
         "metric": "prefix-match blocks/s (batched block hash + prefix match)",
         "value": value, "unit": "blocks/s", "ms_per_step": ms,
-        "config": {**mw.describe(), "instances": world,
+        "scaling": "weak" if world > 1 else None,
+        "config": {**mw.describe(), "instances": 1,
                    "layout": ("one instance index" if world == 1 else
-                              "one prefill instance index per GPU; per-request best combined "
-                              + ("inside the match kernel: atomicMax of packed (len<<32 | ~id) "
-                                 "words into every GPU's result buffer over NVLink, stream-"
-                                 "ordered flags (kvx_xmatch, no collective)"
-                                 if args.match_exchange == "nvlink" else
-                                 "by all-reduce(MAX) over packed (len<<32 | ~id) words (NCCL)"))},
+                              f"data-parallel: each of the {world} GPUs serves its own batch "
+                              "of the trace against its own 1M-key instance index (no "
+                              "exchange; value = all GPUs' blocks / slowest GPU's step)")},
         "kernels": {
             "block_hash_kernel": {
                 "kernel": ("halfwarp_hash_kernel (one CTA per SM; per half-warp one request: "
@@ -929,25 +930,168 @@ def bench_match(args, dev, rank, world, role):
                 # for contents + one per block for the key fold)
                 "compute_roofline": {
                     "bound": "alu (64-bit chain_hash emulated on 32-bit pipes)",
-                    "chain_hashes": int(tok_bytes // 4 + n_blocks),
-                    "achieved_per_s": (tok_bytes // 4 + n_blocks) / (hs["avg_ms"] / 1e3),
+                    "chain_hashes": int(chain_hashes),
+                    "achieved_per_s": chain_hashes / (hs["avg_ms"] / 1e3),
                     "peak_per_s": 760e9,
                     "peak_source": "measured: tests/perf/hash_pipe_micro.cu, full-chip, "
                                    "4 independent chains per thread",
-                    "frac": (tok_bytes // 4 + n_blocks) / (hs["avg_ms"] / 1e3) / 760e9}},
+                    "frac": chain_hashes / (hs["avg_ms"] / 1e3) / 760e9}},
             "match_kernel": {"avg_ms": ms_match["avg_ms"], "probes": n_probes,
                              "bytes": match_bytes, "achieved_gbs": match_gbs,
                              "frac_hbm": match_gbs / peaks["hbm_gbs"],
-                             "note": "24 B per probed block (8 B query + 16 B slot); the 16 MB "
+                             "note": "24 B per probed block (8 B query + 16 B slot); the 32 MiB "
                                      "key array is L2-resident, so frac can exceed 1"}},
         "e2e": {"value": total_blocks / (e2e_ms / 1e3), "unit": "blocks/s",
-                "h2d_bytes_per_step": int(tok_bytes), "d2h_bytes_per_step": mw.n_req * 12},
-        "parity": {"keys_checked": int(n_blocks), "check": "every block key == oracle "
-                   "restatement (oracle/kvx_oracle.c) before timing"},
+                "h2d_bytes_per_step": int(sum_over_ranks(float(tok_bytes + mw.tok_off.nbytes),
+                                                         d)),
+                "d2h_bytes_per_step": int(sum_over_ranks(float(mw.n_req * 12), d)),
+                "path": "python API -> libkvx C ABI: pinned tokens + token offsets H2D, "
+                        "kvx_key_offsets scan, kvx_chain_hash_batch, kvx_match_prefix_batch, "
+                        "best (len, id) D2H, every step"},
+        "parity": {"keys_checked": int(sum_over_ranks(float(n_blocks), d)),
+                   "best_match": match_checked,
+                   "check": "every block key and every request's (best_len, best_id) == oracle "
+                            "restatement (oracle/kvx_oracle.c) over the same 1M-key instance "
+                            "set, before timing; the e2e results are checked too"},
         "cpu_baseline": cpu,
         "pipelined": pipelined,
+        "sharded": sharded,
         "conductor_p8": conductor,
     }
+
+
+def bench_match_sharded(args, dev, rank, world, s, o):
+    """ONE Config 4 batch over `world` GPUs, each GPU one prefill instance
+    (SURVEY 8(e) case (ii)).  Per step: every GPU hashes its token-balanced
+    shard of the requests into its copy of the batch key buffer, pushes it to
+    every peer with the copy engine (kvx_xmatch_share_keys; flags, no
+    collective), then matches the WHOLE batch against its instance with the
+    cross-GPU MAX inside the match kernel (kvx_xmatch_run).  Strong scaling:
+    value = the batch's blocks / slowest GPU's step."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_00079_b200 as pkg
+    from paper_2407_00079_b200.cluster import max_over_ranks
+    from paper_2407_00079_b200.workloads import MatchWorkload
+
+    d = f"cuda:{dev}"
+    mw = MatchWorkload(seed=4).build()  # the same batch on every rank
+    B = Stage1Batch(mw, dev, s)
+    idx = B.index(rank, world)
+    xm = pkg.kvx.XMatch(dev, rank, world, mw.n_req)
+    keys = xm.key_buffer(B.n_blocks)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, xm.export())
+    for blob in blobs:
+        xm.connect(blob)
+    r0, r1 = shard_by_tokens(mw.tok_off, world)[rank]
+    k0, k1 = int(B.key_off_host[r0]), int(B.key_off_host[r1])
+    with torch.cuda.stream(s):
+        best_len = torch.empty(mw.n_req, dtype=torch.int64, device=d)
+        best_id = torch.empty(mw.n_req, dtype=torch.int32, device=d)
+    th = KernelTimer(True)
+
+    def step(timed=False):
+        a = th.start(s) if timed else None
+        pkg.chain_hash_batch(B.tokens, B.tok_off[r0:r1 + 1], mw.block_size,
+                             key_off=B.key_off[r0:r1 + 1], keys=keys, stream=s)
+        th.stop(s, a, (int(mw.tok_off[r1] - mw.tok_off[r0])) * 4 + 8 * (k1 - k0))
+        xm.share_keys(k0, k1, stream=s)
+        xm.run([idx], [rank], keys, B.key_off, out=(best_len, best_id), stream=s)
+
+    for _ in range(args.warmup):
+        step()
+    s.synchronize()
+    k_ref, want_len, want_id = B.oracle_best(o, world)
+    ok = (np.array_equal(keys.cpu().numpy()[: B.n_blocks], k_ref)
+          and np.array_equal(best_len.cpu().numpy(), want_len)
+          and np.array_equal(best_id.cpu().numpy(), want_id))
+    if not ok:
+        raise SystemExit("SHARDED STAGE-1 PARITY FAILURE (keys or best match)")
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(args.steps):
+        step(timed=True)
+    e1.record(s)
+    s.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
+    hs = th.summary()
+    lens = np.diff(mw.tok_off)
+    longest = int((lens.max() + mw.block_size - 1) // mw.block_size)
+    out = {"value": B.n_blocks / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms,
+           "scaling": "strong",
+           "hash_shard_ms_max": max_over_ranks(hs["avg_ms"], d),
+           "layout": f"one 4096-request batch; requests sharded over {world} GPUs by tokens "
+                     "for hashing; keys pushed to every GPU by the copy engine "
+                     "(kvx_xmatch_share_keys); each GPU one prefill instance, global best "
+                     "combined in the match kernel (kvx_xmatch_run)",
+           "longest_request_blocks": longest,
+           "note": "a request's block keys are one sequential chain_hash chain, so the "
+                   "longest request bounds the sharded hash (~1,536 dependent steps)",
+           "parity": {"requests": int(mw.n_req), "mismatched": 0,
+                      "check": "keys and global (best_len, best_id) == oracle over all "
+                               "instances"}}
+    del xm
+    return out
+
+
+def bench_conductor(args, B, keys, s):
+    import torch
+
+    import paper_2407_00079_b200 as pkg
+    from paper_2407_00079_b200 import conductor as cd
+    mw, d = B.mw, keys.device
+    P = 8
+    inst = [B.index(i, P) for i in range(P)]
+    with torch.cuda.stream(s):
+        lens = torch.empty((mw.n_req, P), dtype=torch.int64, device=d)
+        bl8 = torch.empty(mw.n_req, dtype=torch.int64, device=d)
+        bi8 = torch.empty(mw.n_req, dtype=torch.int32, device=d)
+        inp = B.tok_off[1:] - B.tok_off[:-1]
+    rng = np.random.default_rng(8)
+    pre = np.zeros(P, dtype=cd.PREFILL_DT)
+    pre["id"] = np.arange(P)
+    pre["busy_until_ms"] = rng.random(P) * 500
+    pre["sender_busy_until_ms"] = rng.random(P) * 300
+    pre["queued_work_ms"] = rng.random(P) * 1500
+    dec = np.zeros(8, dtype=cd.DECODE_DT)
+    dec["id"] = np.arange(8)
+    dec["batch_size"] = rng.integers(0, 33, 8)
+    dec["resident_kv_tokens"] = rng.integers(0, 200000, 8)
+    perf = cd.PerfParams(cpp_group_size=2)
+    kwargs = dict(perf=perf, l_ttft_ms=30000.0, l_tbt_ms=100.0, threshold=4.0,
+                  block_size=mw.block_size, now_ms=0.0, prefill=pre, decode=dec,
+                  input_len=inp, match_len=lens, stream=s)
+
+    def conduct():
+        pkg.match_prefix_batch(inst, list(range(P)), keys, B.key_off, stream=s,
+                               out=(lens, bl8, bi8))
+        return cd.schedule_batch(**kwargs)
+
+    conduct()
+    s.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(s)
+    for _ in range(args.steps):
+        pkg.match_prefix_batch(inst, list(range(P)), keys, B.key_off, stream=s,
+                               out=(lens, bl8, bi8))
+    c1.record(s)
+    s.synchronize()
+    match8_ms = c0.elapsed_time(c1) / args.steps
+    t0 = time.perf_counter()
+    dec_out = conduct()
+    call_ms = (time.perf_counter() - t0) * 1e3
+    return {
+        "metric": "kvcache-centric schedule of the batch (match matrix + FP64 scoring)",
+        "instances": P, "requests": mw.n_req, "match_matrix_ms": match8_ms,
+        "match_matrix_blocks_per_s": B.n_blocks * P / (match8_ms / 1e3),
+        "end_to_end_call_ms": call_ms,
+        "decisions": {"accepted": int(dec_out["accepted"].sum()),
+                      "migrations": int(dec_out["migrate"].sum())},
+        "note": "scoring bit-identical to kvref::schedule (tests/test_gpu_conductor.py)"}
 
 
 def main():

@@ -88,6 +88,10 @@ int64_t kvx_chain_hash(int64_t prev_key, uint64_t content_hash);
  * producer / fold kernel.  Both are bit-identical. */
 int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req,
                          int64_t bs, const int64_t* d_key_off, int64_t* d_keys, void* stream);
+/* d_key_off[0..n_req] = exclusive scan of ceil((tok_off[r+1]-tok_off[r]) / bs)
+ * (the key offsets kvx_chain_hash_batch takes), on the device. */
+int kvx_key_offsets(const int64_t* d_tok_off, int64_t n_req, int64_t bs, int64_t* d_key_off,
+                    void* stream);
 
 /* ---- stage 1b: block index (GPU open-addressing table) + prefix match ---- */
 
@@ -117,7 +121,10 @@ int kvx_index_stats(kvx_index* idx, int64_t* live, int64_t* tombstones, int64_t*
  *   d_len_out[r*n_inst + i]  match_prefix of request r on instance i (optional)
  *   d_best_len[r], d_best_id[r]  find_best_prefix_match: longest match, ties to
  *                                the lowest inst_ids[i] (conductor.cpp:57-73)
- * n_inst == 0 is KVX_EINVAL (the reference throws on an empty pool).
+ * n_inst == 0 is KVX_EINVAL (the reference throws on an empty pool).  d_keys
+ * may be NULL when every chain is empty (key_off[n_req] == 0): an empty chain
+ * matches 0 blocks everywhere and the best is (0, lowest id), as in the
+ * reference.
  * inst_ids is a HOST array; n_inst <= KVX_MAX_INSTANCES. */
 #define KVX_MAX_INSTANCES 64
 int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
@@ -153,6 +160,17 @@ int kvx_xmatch_connect(kvx_xmatch* x, const uint8_t* blob, int64_t len);
 int kvx_xmatch_run(kvx_xmatch* x, const kvx_index* const* idx, const int32_t* inst_ids,
                    int64_t n_inst, const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
                    int64_t* d_best_len, int32_t* d_best_id, void* stream);
+/* Request-sharded hashing for the same exchange.  kvx_xmatch_key_buffer
+ * (before export/connect; same max_keys on every rank) allocates this rank's
+ * copy of a batch-wide key buffer.  Per step each rank hashes ITS shard of the
+ * requests straight into its copy (kvx_chain_hash_batch with its slice of the
+ * batch's tok_off / key_off: keys land at their batch-wide positions), then
+ * kvx_xmatch_share_keys pushes keys [key_lo, key_hi) into every peer's copy
+ * with the copy engine (NVLink) and makes `stream` wait until every peer's
+ * shard has landed here -- then kvx_xmatch_run on the whole batch, same
+ * stream.  Collective: every rank calls share_keys then run once per step. */
+int kvx_xmatch_key_buffer(kvx_xmatch* x, int64_t max_keys, int64_t** d_keys);
+int kvx_xmatch_share_keys(kvx_xmatch* x, int64_t key_lo, int64_t key_hi, void* stream);
 
 /* ---- batched Conductor scoring (kvcache-centric schedule, FP64) -------- */
 
@@ -261,7 +279,8 @@ int kvx_set_copy_impl(int impl);
  * block) unit whose table entry is outside [0, slots) of its pool -- nothing
  * is written outside a pool -- and flag it on the device.  Synchronizes
  * `stream`, then returns KVX_EINVAL (and clears the flag) if an entry was out
- * of range since the last check on this device, else KVX_OK. */
+ * of range since the last check on the device that owns `stream` (NULL: the
+ * current device), KVX_ECUDA if a pull copy on it timed out, else KVX_OK. */
 int kvx_copy_check(void* stream);
 
 /* ---- stage 3: transfer engine ----------------------------------------- */
@@ -350,6 +369,17 @@ int kvx_streamer_set_timing(kvx_streamer* s, int on, int stride);
 int kvx_streamer_launch_stats(kvx_streamer* s, int64_t* launches, double* avg_ms,
                               double* avg_bytes, int reset);
 uint64_t kvx_streamer_units(const kvx_streamer* s);
+/* Host-blocking: waits for the streamer's queues, then reports a failed unit
+ * since the last check: KVX_ECUDA when a PEER_PULL unit gave up waiting for
+ * the sender (20 s; its decode slots were NOT written and the sender saw bit
+ * 62 in the step's "consumed" word), KVX_EINVAL for out-of-range block-table
+ * entries (kvx_copy_check).  Receivers should call it after a step's finish
+ * before using the decode slots. */
+int kvx_streamer_check(kvx_streamer* s);
+/* 1 when the connected peer process runs on this same GPU (device UUIDs
+ * match): peer modes then wait only with stream memory operations, never
+ * inside a kernel. */
+int kvx_streamer_same_gpu(const kvx_streamer* s);
 /* CUDA-graph record / replay of one step (LOCAL_FUSED only): the sends issued
  * between record_begin and record_end are captured, not run; each replay runs
  * them again with one cudaGraphLaunch on the streamer's queue (tables are read

@@ -82,12 +82,16 @@ def schedule_batch(perf: PerfParams, l_ttft_ms: float, l_tbt_ms: float, threshol
                       perf.epsilon_decode, perf.kv_bytes_per_token, perf.link_bandwidth,
                       perf.load_bandwidth, perf.prefill_chunk, perf.cpp_group_size)
     sp = KvxSchedParams(l_ttft_ms, l_tbt_ms, threshold, now_ms, block_size)
-    d_pre = _dev_bytes(np.ascontiguousarray(prefill, dtype=PREFILL_DT), dev)
-    d_dec = _dev_bytes(np.ascontiguousarray(decode, dtype=DECODE_DT), dev)
+    # the snapshots, the result and its read-back all live on the launch stream
+    # (the caching allocator then never recycles them while the kernel runs)
+    ts = kvx._torch_stream(stream, dev)
     n_req = input_len.numel()
-    out = torch.empty(max(n_req, 1) * DECISION_DT.itemsize, dtype=torch.uint8, device=dev)
-    check(f(C.byref(p), C.byref(sp), d_pre.data_ptr(), len(prefill), d_dec.data_ptr(),
-            len(decode), input_len.data_ptr(), match_len.data_ptr(), n_req, out.data_ptr(),
-            kvx._stream(stream)))
-    host = out.cpu().numpy()
+    with torch.cuda.stream(ts):
+        d_pre = _dev_bytes(np.ascontiguousarray(prefill, dtype=PREFILL_DT), dev)
+        d_dec = _dev_bytes(np.ascontiguousarray(decode, dtype=DECODE_DT), dev)
+        out = torch.empty(max(n_req, 1) * DECISION_DT.itemsize, dtype=torch.uint8, device=dev)
+        check(f(C.byref(p), C.byref(sp), d_pre.data_ptr(), len(prefill), d_dec.data_ptr(),
+                len(decode), input_len.data_ptr(), match_len.data_ptr(), n_req, out.data_ptr(),
+                kvx._stream(ts)))
+        host = out.cpu().numpy()  # a copy on ts: ordered after the kernel, host waits
     return host[: n_req * DECISION_DT.itemsize].view(DECISION_DT)

@@ -405,7 +405,7 @@ std::vector<BestPrefixMatchBatch> find_best_prefix_match_batch(
     gpu::cuda_ok(cudaMemcpyAsync(d_keys, keys.data(), nk * sizeof(int64_t),
                                  cudaMemcpyHostToDevice, s), "H2D keys");
   gpu::ok(kvx_match_prefix_batch(idx.data(), ids.data(), static_cast<int64_t>(n_inst),
-                                 nk ? d_keys : nullptr, d_off, static_cast<int64_t>(n_req),
+                                 d_keys, d_off, static_cast<int64_t>(n_req),
                                  per_instance ? d_len : nullptr, d_best, d_bid, s),
           "kvx_match_prefix_batch");
   std::vector<int64_t> best(n_req);

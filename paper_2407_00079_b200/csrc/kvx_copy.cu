@@ -201,37 +201,64 @@ __global__ void __launch_bounds__(kLsuThreads, 2) copy_lsu_kernel(const SlabCopy
   lsu_copy<true, true, Idx>(c);
 }
 
-// Pull copy of one layer-wise unit whose readiness flag is checked in the
-// kernel (PEER_PULL receiver): thread 0 waits until the sender's flag reaches
-// `value` (system-scope acquire; the sender's stream write fences the unit's
-// KV first), the CTA follows through the barrier, and only then are
-// dependents released -- so with programmatic dependent launch at most the
-// next unit waits ahead of the data.  Gives up after 20 s (g_wait_timeouts;
-// kvx_copy_check reports it) instead of hanging the GPU.
-template <class Idx>
-__global__ void __launch_bounds__(kLsuThreads, 2) copy_pull_kernel(
-    const SlabCopy c, const unsigned long long* __restrict__ flag, unsigned long long value) {
-  __shared__ int go;
+// PEER_PULL receiver, one layer-wise unit = a one-warp gate kernel + the pull
+// copy launched programmatically dependent on it.  The gate waits for the
+// sender's readiness flag (system-scope acquire; the sender's stream write
+// fences the unit's KV first) and only then releases the copy, so while the
+// decode GPU waits for a slow prefill exactly ONE warp is resident -- the
+// copy's CTAs are not scheduled ahead of their data (they would otherwise
+// occupy every SM and starve decode kernels).  The gate itself is launched
+// programmatically dependent on the previous unit's copy, so in steady state
+// it has already passed when that copy drains and unit k+1 ramps up while unit
+// k finishes.  Gives up after 20 s: *status (the streamer's failure word) and
+// g_wait_timeouts are set, the copies skip, kvx_streamer_check /
+// kvx_copy_check report it instead of the GPU hanging.
+__global__ void __launch_bounds__(32) pull_gate_kernel(const unsigned long long* __restrict__ flag,
+                                                       unsigned long long value,
+                                                       unsigned long long* __restrict__ status) {
   if (threadIdx.x == 0) {
     unsigned long long t0, t, v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    int ok = 1;
+    unsigned ns = 32;
     while (true) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
       if (v >= value) break;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       if (t - t0 > 20000000000ull) {
-        ok = 0;
+        *status = 1;
         g_wait_timeouts = 1;
         break;
       }
-      __nanosleep(256);
+      __nanosleep(ns);
+      ns = ns < 1024 ? 2 * ns : ns;
     }
-    go = ok;
   }
-  __syncthreads();
-  asm volatile("griddepcontrol.launch_dependents;");
-  if (go) lsu_copy<true, true, Idx, true>(c);
+  __syncwarp();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// The pull copy: coherent loads of the peer pool (another GPU wrote it while
+// this grid may already have been launched), evict-first local stores.  It
+// first waits for its gate to complete (griddepcontrol.wait: no-op for a plain
+// launch) and then lets the next unit's gate be scheduled.
+template <class Idx>
+__global__ void __launch_bounds__(kLsuThreads, 2) copy_pull_kernel(
+    const SlabCopy c, const unsigned long long* __restrict__ status) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (status && *reinterpret_cast<const volatile unsigned long long*>(status)) return;
+  lsu_copy<true, true, Idx, true>(c);
+}
+
+// Receiver -> sender "source blocks consumed" word of a PEER_PULL step: the
+// consumed unit count, with bit 62 set when a unit of the step timed out (the
+// sender's GEQ wait passes either way; the receiver's host sees the failure
+// through kvx_streamer_check).
+__global__ void pull_done_kernel(const unsigned long long* __restrict__ status,
+                                 unsigned long long* __restrict__ peer_flag,
+                                 unsigned long long value) {
+  const unsigned long long v = *status ? (value | (1ull << 62)) : value;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_flag), "l"(v) : "memory");
 }
 
 // ---- TMA bulk-copy pipeline ----------------------------------------------
@@ -693,14 +720,49 @@ int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* ds
 }  // extern "C"
 
 namespace kvx {
+namespace {
+cudaLaunchAttribute pdl_attr() {
+  cudaLaunchAttribute a;
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = 1;
+  return a;
+}
+}  // namespace
+
+int pull_gate(const uint64_t* d_flag, uint64_t value, uint64_t* d_status, void* stream,
+              bool overlap_prev) {
+  KVX_REQUIRE(d_flag && d_status, "pull_gate: NULL flag or status");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1] = {pdl_attr()};
+  cfg.attrs = overlap_prev ? attr : nullptr;
+  cfg.numAttrs = overlap_prev ? 1 : 0;
+  KVX_CUDA(cudaLaunchKernelEx(&cfg, pull_gate_kernel,
+                              reinterpret_cast<const unsigned long long*>(d_flag),
+                              static_cast<unsigned long long>(value),
+                              reinterpret_cast<unsigned long long*>(d_status)));
+  KVX_LAUNCH_CHECK("pull_gate_kernel");
+  return KVX_OK;
+}
+
+int pull_done(const uint64_t* d_status, uint64_t* d_peer_flag, uint64_t value, void* stream) {
+  KVX_REQUIRE(d_status && d_peer_flag, "pull_done: NULL status or flag");
+  pull_done_kernel<<<1, 1, 0, as_stream(stream)>>>(
+      reinterpret_cast<const unsigned long long*>(d_status),
+      reinterpret_cast<unsigned long long*>(d_peer_flag), static_cast<unsigned long long>(value));
+  KVX_LAUNCH_CHECK("pull_done_kernel");
+  return KVX_OK;
+}
+
 int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
                     const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, void* stream,
-                    const uint64_t* d_flag, uint64_t value, bool overlap_prev) {
+                    const uint64_t* d_status, bool after_gate) {
   SlabCopy c;
   bool empty = false;
   const int st = paged_copy_args(src, d_src_table, dst, d_dst_table, n, lo, hi, &c, &empty);
   if (st || empty) return st;
-  KVX_REQUIRE(d_flag, "copy_paged_pull: NULL flag");
   const int dev = dst->d.device;  // the pulling GPU
   DeviceGuard g(dev);
   const int64_t items = c.planes * c.n * ((c.slab + kLsuItem - 1) / kLsuItem);
@@ -709,17 +771,14 @@ int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* d
   cfg.gridDim = dim3(blocks);
   cfg.blockDim = dim3(kLsuThreads);
   cfg.stream = as_stream(stream);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = overlap_prev ? attr : nullptr;
-  cfg.numAttrs = overlap_prev ? 1 : 0;
-  const auto* f = reinterpret_cast<const unsigned long long*>(d_flag);
-  const unsigned long long v = value;
+  cudaLaunchAttribute attr[1] = {pdl_attr()};
+  cfg.attrs = after_gate ? attr : nullptr;
+  cfg.numAttrs = after_gate ? 1 : 0;
+  const auto* f = reinterpret_cast<const unsigned long long*>(d_status);
   if (items + blocks < (int64_t{1} << 32))
-    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<uint32_t>, c, f, v));
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<uint32_t>, c, f));
   else
-    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<int64_t>, c, f, v));
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<int64_t>, c, f));
   KVX_LAUNCH_CHECK("copy_pull_kernel");
   return KVX_OK;
 }
@@ -739,6 +798,14 @@ int copy_paged_overlapped(const kvx_pool* src, const int32_t* d_src_table, kvx_p
 extern "C" {
 
 int kvx_copy_check(void* stream) {
+  // the flags are per device: read the ones of the device that owns `stream`
+  int dev = -1;
+  if (stream) {
+    KVX_CUDA(cudaStreamGetDevice(as_stream(stream), &dev));
+  } else {
+    KVX_CUDA(cudaGetDevice(&dev));
+  }
+  DeviceGuard g(dev);
   KVX_CUDA(cudaStreamSynchronize(as_stream(stream)));
   unsigned long long timeouts = 0, bad = 0, zero = 0;
   KVX_CUDA(cudaMemcpyFromSymbol(&timeouts, g_wait_timeouts, sizeof(timeouts)));

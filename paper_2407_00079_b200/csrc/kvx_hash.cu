@@ -128,10 +128,11 @@ __global__ void __launch_bounds__(256) block_hash_prep_kernel(const int64_t* __r
                                                               int64_t n_req,
                                                               int64_t* __restrict__ keys,
                                                               unsigned long long* __restrict__ ws) {
-  const int64_t total = key_off[n_req];
+  // key_off may be a slice of a larger batch (absolute positions)
+  const int64_t first = key_off[0], total = key_off[n_req];
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = tid; i < total; i += stride) keys[i] = -1;
+  for (int64_t i = first + tid; i < total; i += stride) keys[i] = -1;
   unsigned long long wmax = 0;
   for (int64_t r = tid; r < n_req; r += stride) {
     const auto w = static_cast<unsigned long long>((key_off[r + 1] - key_off[r] + 31) / 32);
@@ -630,7 +631,73 @@ Workspace& workspace() {
 }  // namespace
 }  // namespace kvx
 
+namespace kvx {
+namespace {
+// key_off = exclusive scan of ceil((tok_off[r+1] - tok_off[r]) / bs): one CTA,
+// 1024 threads x 8 requests per pass, warp-shuffle scans, a running carry
+// (4,096 requests = one pass; the launch is latency, not bandwidth, bound).
+constexpr int kScanThreads = 1024, kScanPer = 8;
+__global__ void __launch_bounds__(kScanThreads) key_offsets_kernel(
+    const int64_t* __restrict__ tok_off, int64_t n_req, int64_t bs, int64_t* __restrict__ key_off) {
+  __shared__ int64_t warp_tot[kScanThreads / 32];
+  __shared__ int64_t carry_s;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n_req; base += int64_t{kScanThreads} * kScanPer) {
+    int64_t v[kScanPer];
+    int64_t mine = 0;
+    const int64_t r0 = base + static_cast<int64_t>(threadIdx.x) * kScanPer;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      const int64_t r = r0 + j;
+      v[j] = r < n_req ? (tok_off[r + 1] - tok_off[r] + bs - 1) / bs : 0;
+      mine += v[j];
+    }
+    int64_t incl = mine;  // inclusive scan over the warp
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = warp_tot[lane], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+      }
+      warp_tot[lane] = wi - w;  // exclusive prefix of the warps
+    }
+    __syncthreads();
+    int64_t run = carry_s + warp_tot[warp] + incl - mine;
+#pragma unroll
+    for (int j = 0; j < kScanPer; ++j) {
+      const int64_t r = r0 + j;
+      if (r < n_req) key_off[r] = run;
+      run += v[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == kScanThreads - 1) carry_s = run;  // last thread holds the pass total
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) key_off[n_req] = carry_s;
+}
+}  // namespace
+}  // namespace kvx
+
 using namespace kvx;
+
+extern "C" int kvx_key_offsets(const int64_t* d_tok_off, int64_t n_req, int64_t bs,
+                               int64_t* d_key_off, void* stream) {
+  KVX_REQUIRE(n_req >= 0 && bs >= 1, "kvx_key_offsets: bad n_req / block size");
+  KVX_REQUIRE(d_tok_off && d_key_off, "kvx_key_offsets: NULL array");
+  key_offsets_kernel<<<1, kScanThreads, 0, as_stream(stream)>>>(d_tok_off, n_req, bs, d_key_off);
+  KVX_LAUNCH_CHECK("key_offsets_kernel");
+  return KVX_OK;
+}
 
 extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_tok_off,
                                     int64_t n_req, int64_t bs, const int64_t* d_key_off,

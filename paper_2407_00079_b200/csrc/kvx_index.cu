@@ -543,7 +543,9 @@ int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids,
   KVX_REQUIRE((d_best_len == nullptr) == (d_best_id == nullptr),
               "kvx_match_prefix_batch: best_len and best_id go together");
   if (n_req == 0) return KVX_OK;
-  KVX_REQUIRE(d_keys && d_key_off, "kvx_match_prefix_batch: NULL keys");
+  // d_keys may be NULL when every chain is empty (the kernel reads keys only
+  // inside a request's [key_off[r], key_off[r+1]) range)
+  KVX_REQUIRE(d_key_off, "kvx_match_prefix_batch: NULL key offsets");
   return match_impl(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out, d_best_len,
                     d_best_id, false, stream);
 }
@@ -556,7 +558,7 @@ int kvx_match_prefix_packed(const kvx_index* const* idx, const int32_t* inst_ids
   KVX_REQUIRE(idx != nullptr && inst_ids != nullptr, "kvx_match_prefix_packed: NULL instances");
   KVX_REQUIRE(n_req >= 0, "kvx_match_prefix_packed: n_req must be >= 0");
   if (n_req == 0) return KVX_OK;
-  KVX_REQUIRE(d_keys && d_key_off && d_packed, "kvx_match_prefix_packed: NULL array");
+  KVX_REQUIRE(d_key_off && d_packed, "kvx_match_prefix_packed: NULL array");
   return match_impl(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, nullptr,
                     reinterpret_cast<int64_t*>(d_packed), nullptr, true, stream);
 }
@@ -625,17 +627,36 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
 // buffered by step parity: a rank zeroes the buffer for step e+1 before it
 // announces step e, and every rank starts step e+1 only after all step-e
 // announcements, so no atomic can hit a buffer before it was zeroed.
+//
+// Request-sharded hashing (kvx_xmatch_key_buffer / kvx_xmatch_share_keys):
+// every rank hashes only its shard of the batch into its copy of a shared key
+// buffer, then copy-engine pushes that shard into every peer's copy (CUDA IPC)
+// and raises a per-rank "keys of step e landed" flag there; each rank's
+// stream waits for all peers' flags before its match.  A rank's pushes of
+// step e+1 are queued after its xmatch_run of step e, which waited for every
+// rank's step-e announcement (written after that rank's match kernel), so no
+// push can overwrite keys a peer is still matching.
 struct kvx_xmatch {
   int device = 0, rank = 0, world = 1;
   int64_t max_req = 0;
-  uint8_t* mem = nullptr;  // [buf0 | buf1 | flags[KVX_MAX_PEERS]]
+  uint8_t* mem = nullptr;  // [buf0 | buf1 | flags[KVX_MAX_PEERS] | keyflags[KVX_MAX_PEERS]]
   uint64_t* peer_buf[KVX_MAX_PEERS][2] = {};
   uint64_t* peer_flags[KVX_MAX_PEERS] = {};
   void* peer_mem[KVX_MAX_PEERS] = {};
   uint64_t epoch = 0;
+  // shared key buffer (optional)
+  int64_t max_keys = 0;
+  int64_t* keys = nullptr;
+  int64_t* peer_keys[KVX_MAX_PEERS] = {};
+  uint64_t key_epoch = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_dep = nullptr;
   uint64_t* buf(int b) const { return reinterpret_cast<uint64_t*>(mem) + b * max_req; }
   uint64_t* flags() const { return reinterpret_cast<uint64_t*>(mem) + 2 * max_req; }
-  size_t bytes() const { return (2 * static_cast<size_t>(max_req) + KVX_MAX_PEERS) * sizeof(uint64_t); }
+  uint64_t* keyflags() const { return flags() + KVX_MAX_PEERS; }
+  size_t bytes() const {
+    return (2 * static_cast<size_t>(max_req) + 2 * KVX_MAX_PEERS) * sizeof(uint64_t);
+  }
 };
 
 namespace {
@@ -643,6 +664,8 @@ struct XmatchBlob {
   int32_t magic, rank, world, pad;
   int64_t max_req;
   uint8_t handle[KVX_IPC_HANDLE_BYTES];
+  int64_t max_keys;  // 0: no shared key buffer
+  uint8_t key_handle[KVX_IPC_HANDLE_BYTES];
 };
 constexpr int32_t kXmatchMagic = 0x6b76786d;  // "kvxm"
 }  // namespace
@@ -678,8 +701,13 @@ int kvx_xmatch_destroy(kvx_xmatch* x) {
   if (!x) return KVX_OK;
   DeviceGuard g(x->device);
   cudaDeviceSynchronize();
-  for (int j = 0; j < KVX_MAX_PEERS; ++j)
+  for (int j = 0; j < KVX_MAX_PEERS; ++j) {
     if (x->peer_mem[j]) kvx_ipc_close(x->peer_mem[j]);
+    if (x->peer_keys[j] && j != x->rank) kvx_ipc_close(x->peer_keys[j]);
+  }
+  if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
+  if (x->copy_dep) cudaEventDestroy(x->copy_dep);
+  if (x->keys) cudaFree(x->keys);
   if (x->mem) cudaFree(x->mem);
   delete x;
   return KVX_OK;
@@ -697,6 +725,11 @@ int kvx_xmatch_export(kvx_xmatch* x, uint8_t* blob, int64_t cap, int64_t* len) {
   b.max_req = x->max_req;
   int rc = kvx_ipc_export(x->mem, b.handle);
   if (rc) return rc;
+  b.max_keys = x->max_keys;
+  if (x->keys) {
+    rc = kvx_ipc_export(x->keys, b.key_handle);
+    if (rc) return rc;
+  }
   std::memcpy(blob, &b, sizeof(b));
   return KVX_OK;
 }
@@ -707,8 +740,8 @@ int kvx_xmatch_connect(kvx_xmatch* x, const uint8_t* blob, int64_t len) {
   XmatchBlob b;
   std::memcpy(&b, blob, sizeof(b));
   KVX_REQUIRE(b.magic == kXmatchMagic && b.world == x->world && b.max_req == x->max_req &&
-                  b.rank >= 0 && b.rank < x->world,
-              "kvx_xmatch_connect: peer does not match");
+                  b.rank >= 0 && b.rank < x->world && b.max_keys == x->max_keys,
+              "kvx_xmatch_connect: peer does not match (rank / world / max_req / key buffer)");
   if (b.rank == x->rank) return KVX_OK;  // self
   KVX_REQUIRE(x->peer_mem[b.rank] == nullptr, "kvx_xmatch_connect: peer already connected");
   void* p = nullptr;
@@ -719,6 +752,62 @@ int kvx_xmatch_connect(kvx_xmatch* x, const uint8_t* blob, int64_t len) {
   x->peer_buf[b.rank][0] = words;
   x->peer_buf[b.rank][1] = words + x->max_req;
   x->peer_flags[b.rank] = words + 2 * x->max_req;
+  if (x->max_keys) {
+    rc = kvx_ipc_open(b.key_handle, x->device, &p);
+    if (rc) return rc;
+    x->peer_keys[b.rank] = static_cast<int64_t*>(p);
+  }
+  return KVX_OK;
+}
+
+int kvx_xmatch_key_buffer(kvx_xmatch* x, int64_t max_keys, int64_t** d_keys) {
+  KVX_REQUIRE(x && d_keys && max_keys >= 1, "kvx_xmatch_key_buffer: bad arguments");
+  if (x->keys) {
+    KVX_REQUIRE(max_keys <= x->max_keys, "kvx_xmatch_key_buffer: already sized smaller");
+    *d_keys = x->keys;
+    return KVX_OK;
+  }
+  for (int j = 0; j < x->world; ++j)
+    KVX_REQUIRE(j == x->rank || x->peer_mem[j] == nullptr,
+                "kvx_xmatch_key_buffer: call before exporting / connecting");
+  DeviceGuard g(x->device);
+  KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&x->keys), sizeof(int64_t) * max_keys));
+  KVX_CUDA(cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking));
+  KVX_CUDA(cudaEventCreateWithFlags(&x->copy_dep, cudaEventDisableTiming));
+  x->max_keys = max_keys;
+  x->peer_keys[x->rank] = x->keys;
+  *d_keys = x->keys;
+  return KVX_OK;
+}
+
+int kvx_xmatch_share_keys(kvx_xmatch* x, int64_t key_lo, int64_t key_hi, void* stream) {
+  KVX_REQUIRE(x && x->keys, "kvx_xmatch_share_keys: no key buffer");
+  KVX_REQUIRE(0 <= key_lo && key_lo <= key_hi && key_hi <= x->max_keys,
+              "kvx_xmatch_share_keys: key range out of the buffer");
+  for (int j = 0; j < x->world; ++j)
+    KVX_REQUIRE(x->peer_keys[j] != nullptr, "kvx_xmatch_share_keys: not connected to every rank");
+  DeviceGuard g(x->device);
+  const uint64_t e = ++x->key_epoch;
+  // the pushes follow this rank's hash of its shard (queued on `stream`)
+  KVX_CUDA(cudaEventRecord(x->copy_dep, as_stream(stream)));
+  KVX_CUDA(cudaStreamWaitEvent(x->copy_stream, x->copy_dep, 0));
+  const size_t bytes = sizeof(int64_t) * static_cast<size_t>(key_hi - key_lo);
+  for (int k = 1; k < x->world; ++k) {  // start with the next rank: spread the pushes
+    const int j = (x->rank + k) % x->world;
+    if (bytes)
+      KVX_CUDA(cudaMemcpyAsync(x->peer_keys[j] + key_lo, x->keys + key_lo, bytes,
+                               cudaMemcpyDefault, x->copy_stream));
+  }
+  for (int k = 1; k < x->world; ++k) {  // "my shard of step e landed" (after the copies)
+    const int j = (x->rank + k) % x->world;
+    int rc = kvx_signal_write(x->copy_stream, x->peer_flags[j] + KVX_MAX_PEERS + x->rank, e);
+    if (rc) return rc;
+  }
+  for (int j = 0; j < x->world; ++j) {  // every peer's shard is here before the match
+    if (j == x->rank) continue;
+    int rc = kvx_signal_wait(stream, x->keyflags() + j, e);
+    if (rc) return rc;
+  }
   return KVX_OK;
 }
 
@@ -730,7 +819,7 @@ int kvx_xmatch_run(kvx_xmatch* x, const kvx_index* const* idx, const int32_t* in
   KVX_REQUIRE(n_inst <= KVX_MAX_INSTANCES, "kvx_xmatch_run: too many instances");
   KVX_REQUIRE(idx != nullptr && inst_ids != nullptr, "kvx_xmatch_run: NULL instances");
   KVX_REQUIRE(n_req >= 0 && n_req <= x->max_req, "kvx_xmatch_run: n_req out of range");
-  KVX_REQUIRE(d_keys && d_key_off && d_best_len && d_best_id, "kvx_xmatch_run: NULL array");
+  KVX_REQUIRE(d_key_off && d_best_len && d_best_id, "kvx_xmatch_run: NULL array");
   for (int j = 0; j < x->world; ++j)
     KVX_REQUIRE(x->peer_buf[j][0] != nullptr, "kvx_xmatch_run: not connected to every rank");
   DeviceGuard g(x->device);

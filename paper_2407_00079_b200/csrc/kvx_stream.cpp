@@ -16,12 +16,17 @@
 //   PEER_FUSED    sender kernel stores straight into the receiver's pool (IPC view)
 //   PEER_PULL     receiver kernel loads the sender's pool (IPC view) over NVLink
 //                 and stores into its own pool; per-unit readiness flags from the
-//                 sender; the prefill GPU's SMs stay free
+//                 sender, each unit released by a one-warp gate kernel; the
+//                 prefill GPU's SMs stay free
 //   PEER_CE       sender gathers into a ring slot, the copy engine moves it into
 //                 the receiver's ring (IPC), the receiver scatters; 64-bit flags
 //                 written with stream memory operations order the three queues
 //                 across processes (no kernel ever spins on another's flag).
 // Sequence numbers only grow, so flags never need resetting (no ABA).
+// The two ends may also be two processes on ONE GPU (same device UUID in the
+// handshake): then no kernel ever waits for the other process -- every wait is
+// a stream memory operation -- because nothing guarantees that kernels of two
+// processes sharing a GPU run at the same time.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -50,6 +55,9 @@ struct kvx_streamer {
   std::vector<cudaEvent_t> slot_ev;  // LOCAL_STAGED: scatter that last read each slot
   std::vector<cudaEvent_t> gather_ev;
   uint64_t* flag = nullptr;          // local 64-bit flag word (peer writes it)
+  uint64_t* pull_status = nullptr;   // PEER_PULL receiver: nonzero once a unit's gate timed out
+  bool same_gpu = false;             // the peer process runs on this very GPU
+  bool gate_kernel = false;          // PEER_PULL receiver: units released by the gate kernel
   uint64_t* peer_flag = nullptr;     // the peer's flag word, mapped here
   kvx_pool* peer_view = nullptr;     // PEER_FUSED: receiver's pool as seen by the sender
   uint64_t seq = 0;                  // units issued (sender) / consumed (receiver)
@@ -120,6 +128,23 @@ bool pdl_enabled() {
   return on;
 }
 
+int device_uuid(int dev, uint8_t out[16]) {
+  cudaDeviceProp p;
+  KVX_CUDA(cudaGetDeviceProperties(&p, dev));
+  std::memcpy(out, &p.uuid, 16);
+  return KVX_OK;
+}
+
+// KVX_PULL_GATE=stream: release PEER_PULL units with stream waits instead of
+// the gate kernel (measurement knob; always so when both ends share a GPU).
+bool pull_gate_kernel_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("KVX_PULL_GATE");
+    return !(e && std::strcmp(e, "stream") == 0);
+  }();
+  return on;
+}
+
 bool is_peer(const kvx_streamer* s) {
   return s->d.mode == KVX_STREAM_PEER_FUSED || s->d.mode == KVX_STREAM_PEER_CE ||
          s->d.mode == KVX_STREAM_PEER_PULL;
@@ -133,6 +158,7 @@ struct ExportBlob {
   int64_t slot_bytes;
   uint8_t flag[KVX_IPC_HANDLE_BYTES];
   uint8_t pool[KVX_IPC_HANDLE_BYTES];
+  uint8_t uuid[16];  // the exporting GPU (two processes may share one GPU)
   // followed by ring * KVX_IPC_HANDLE_BYTES slot handles
 };
 constexpr int32_t kMagic = 0x6b767873;  // "kvxs"
@@ -190,6 +216,7 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
   if (is_peer(s)) {
     e = cudaMalloc(reinterpret_cast<void**>(&s->flag), 256);
     if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: flag"));
+    s->pull_status = s->flag + 8;  // same allocation, not written by the peer
     e = cudaMemsetAsync(s->flag, 0, 256, s->s_main);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s->s_main);  // zero before the peer maps it
     if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: flag"));
@@ -249,7 +276,9 @@ int kvx_streamer_export(kvx_streamer* s, uint8_t* blob, int64_t cap, int64_t* le
   b.mode = s->d.mode;
   b.ring = static_cast<int32_t>(s->ring.size());
   b.slot_bytes = s->d.slot_bytes;
-  int rc = kvx_ipc_export(s->flag, b.flag);
+  int rc = device_uuid(s->device, b.uuid);
+  if (rc) return rc;
+  rc = kvx_ipc_export(s->flag, b.flag);
   if (rc) return rc;
   if (s->d.role == KVX_ROLE_RECEIVER && s->d.mode == KVX_STREAM_PEER_FUSED) {
     rc = kvx_ipc_export(kvx_pool_base(s->dst), b.pool);
@@ -277,8 +306,13 @@ int kvx_streamer_connect(kvx_streamer* s, const uint8_t* blob, int64_t len,
   std::memcpy(&b, blob, sizeof(b));
   KVX_REQUIRE(b.magic == kMagic && b.mode == s->d.mode, "kvx_streamer_connect: peer mismatch");
   kvx::DeviceGuard g(s->device);
+  uint8_t mine[16];
+  int rc = device_uuid(s->device, mine);
+  if (rc) return rc;
+  s->same_gpu = std::memcmp(mine, b.uuid, 16) == 0;
+  s->gate_kernel = !s->same_gpu && pull_gate_kernel_enabled();
   void* p = nullptr;
-  int rc = kvx_ipc_open(b.flag, s->device, &p);
+  rc = kvx_ipc_open(b.flag, s->device, &p);
   if (rc) return rc;
   s->peer_flag = static_cast<uint64_t*>(p);
   const bool maps_pool = (s->d.role == KVX_ROLE_SENDER && s->d.mode == KVX_STREAM_PEER_FUSED) ||
@@ -433,26 +467,30 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t
       KVX_REQUIRE(d_dst_table, "kvx_streamer_recv: NULL table");
       if (s->d.mode == KVX_STREAM_PEER_PULL) {
         KVX_REQUIRE(d_src_table && s->peer_view, "kvx_streamer_recv: pull needs the src table");
-        // After the first unit of a call, the pull kernel waits for the
-        // sender's flag itself and is launched programmatically dependent, so
-        // unit c+1 ramps up while unit c drains; the first unit (and a launch
-        // sampled for timing) waits on the stream instead and runs isolated.
-        const bool in_kernel = pdl_enabled() && !first_unit && !will_sample(s);
-        first_unit = false;
+        // Unit c is released by the sender's flag reaching c + 1.  Across two
+        // GPUs a one-warp gate kernel waits for it and the copy launches
+        // programmatically dependent on the gate; the gate of a unit after
+        // the first of a call is itself dependent on the previous unit's copy,
+        // so unit c+1 ramps up while unit c drains, yet only the gate is
+        // resident while the data is not there.  On a shared GPU (or with
+        // KVX_PULL_GATE=stream) the stream front end waits instead.  A launch
+        // sampled for timing runs isolated.
+        const bool sampled = will_sample(s);
+        const bool pdl = pdl_enabled();
         int rc = KVX_OK;
-        if (in_kernel) {
-          rc = timed_launch(s, s->s_main, 1.0 * payload, [&] {
-            return kvx::copy_paged_pull(s->peer_view, d_src_table + b0, s->dst, d_dst_table + b0,
-                                        nb, l0, l1, s->s_main, s->flag, c + 1, true);
-          });
-          if (rc) return rc;
-          continue;
+        bool after_gate = false;
+        if (s->gate_kernel) {
+          rc = kvx::pull_gate(s->flag, c + 1, s->pull_status, s->s_main,
+                              pdl && !first_unit && !sampled);
+          after_gate = pdl && !sampled;
+        } else {
+          rc = kvx_signal_wait(s->s_main, s->flag, c + 1);
         }
-        rc = kvx_signal_wait(s->s_main, s->flag, c + 1);  // sender: unit c is ready
+        first_unit = false;
         if (rc) return rc;
         rc = timed_launch(s, s->s_main, 1.0 * payload, [&] {
-          return kvx_copy_paged(s->peer_view, d_src_table + b0, s->dst, d_dst_table + b0, nb, l0,
-                                l1, s->s_main);
+          return kvx::copy_paged_pull(s->peer_view, d_src_table + b0, s->dst, d_dst_table + b0, nb,
+                                      l0, l1, s->s_main, s->pull_status, after_gate);
         });
         if (rc) return rc;
         continue;
@@ -481,9 +519,12 @@ int kvx_streamer_finish(kvx_streamer* s, void* stream) {
                                           : kvx_signal_wait(s->s_main, s->flag, s->seq);
     if (rc) return rc;
   }
-  if (s->d.mode == KVX_STREAM_PEER_PULL) {  // receiver -> sender: source blocks consumed
-    int rc = s->d.role == KVX_ROLE_RECEIVER ? kvx_signal_write(s->s_main, s->peer_flag, s->seq)
-                                            : kvx_signal_wait(s->s_main, s->flag, s->seq);
+  if (s->d.mode == KVX_STREAM_PEER_PULL) {
+    // receiver -> sender: source blocks consumed (bit 62 set if a unit timed
+    // out; the receiver's host learns it from kvx_streamer_check)
+    int rc = s->d.role == KVX_ROLE_RECEIVER
+                 ? kvx::pull_done(s->pull_status, s->peer_flag, s->seq, s->s_main)
+                 : kvx_signal_wait(s->s_main, s->flag, s->seq);
     if (rc) return rc;
   }
   if (stream) {
@@ -600,5 +641,27 @@ int kvx_streamer_set_timing(kvx_streamer* s, int on, int stride) {
 }
 
 uint64_t kvx_streamer_units(const kvx_streamer* s) { return s ? s->seq : 0; }
+
+int kvx_streamer_check(kvx_streamer* s) {
+  KVX_REQUIRE(s != nullptr, "kvx_streamer_check: NULL");
+  kvx::DeviceGuard g(s->device);
+  KVX_CUDA(cudaStreamSynchronize(s->s_main));
+  if (s->s_second) KVX_CUDA(cudaStreamSynchronize(s->s_second));
+  if (s->xfer) KVX_CUDA(cudaStreamSynchronize(as_stream(kvx_xfer_stream(s->xfer))));
+  if (s->pull_status && s->d.role == KVX_ROLE_RECEIVER) {
+    uint64_t st = 0;
+    KVX_CUDA(cudaMemcpy(&st, s->pull_status, sizeof(st), cudaMemcpyDeviceToHost));
+    if (st) {
+      KVX_CUDA(cudaMemset(s->pull_status, 0, sizeof(st)));
+      kvx_copy_check(s->s_main);  // clears the device-wide timeout flag too
+      return set_error(KVX_ECUDA,
+                       "kvx_streamer_check: a pulled unit timed out waiting for the sender "
+                       "(20 s); its decode slots were not written");
+    }
+  }
+  return kvx_copy_check(s->s_main);
+}
+
+int kvx_streamer_same_gpu(const kvx_streamer* s) { return s && s->same_gpu ? 1 : 0; }
 
 }  // extern "C"

@@ -89,6 +89,9 @@ _sig("kvx_launch_count", C.c_uint64)
 _sig("kvx_sync", C.c_int, _vp)
 _sig("kvx_chain_hash", _i64, _i64, C.c_uint64)
 _sig("kvx_chain_hash_batch", C.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp)
+_sig("kvx_key_offsets", C.c_int, _vp, _i64, _i64, _vp, _vp)
+_sig("kvx_xmatch_key_buffer", C.c_int, _vp, _i64, C.POINTER(_vp))
+_sig("kvx_xmatch_share_keys", C.c_int, _vp, _i64, _i64, _vp)
 _sig("kvx_index_create", C.c_int, C.c_int, _i64, C.POINTER(_vp))
 _sig("kvx_index_destroy", C.c_int, _vp)
 _sig("kvx_index_device", C.c_int, _vp)
@@ -223,11 +226,14 @@ def chain_hash(prev_key: int, content_hash: int) -> int:
     return int(_L.kvx_chain_hash(int(prev_key), int(content_hash) & 0xFFFFFFFFFFFFFFFF))
 
 
-def key_offsets(tok_off: torch.Tensor, bs: int) -> torch.Tensor:
-    lens = tok_off[1:] - tok_off[:-1]
-    blocks = (lens + bs - 1) // bs
-    out = torch.zeros(len(tok_off), dtype=torch.int64, device=tok_off.device)
-    torch.cumsum(blocks, 0, out=out[1:])
+def key_offsets(tok_off: torch.Tensor, bs: int, out: Optional[torch.Tensor] = None,
+                stream=None) -> torch.Tensor:
+    """Exclusive scan of ceil(len/bs) per request (kvx_key_offsets kernel)."""
+    assert tok_off.dtype == torch.int64
+    with torch.cuda.stream(_torch_stream(stream, tok_off.device)):
+        if out is None:
+            out = torch.empty(len(tok_off), dtype=torch.int64, device=tok_off.device)
+    check(_L.kvx_key_offsets(_ptr(tok_off), len(tok_off) - 1, bs, _ptr(out), _stream(stream)))
     return out
 
 
@@ -240,7 +246,7 @@ def chain_hash_batch(tokens: torch.Tensor, tok_off: torch.Tensor, bs: int,
     # the offsets and the output are made on the stream the kernel runs on
     with torch.cuda.stream(_torch_stream(stream, tokens.device)):
         if key_off is None:
-            key_off = key_offsets(tok_off, bs)
+            key_off = key_offsets(tok_off, bs, stream=stream)
         if keys is None:
             n_keys = int(key_off[-1].item())
             keys = torch.empty(max(n_keys, 1), dtype=torch.int64, device=tokens.device)[:n_keys]
@@ -358,6 +364,19 @@ class XMatch:
 
     def connect(self, blob: bytes) -> None:
         check(_L.kvx_xmatch_connect(self.h, blob, len(blob)))
+
+    def key_buffer(self, max_keys: int) -> torch.Tensor:
+        """This rank's copy of the batch-wide key buffer (request-sharded
+        hashing); call before export()."""
+        p = _vp()
+        check(_L.kvx_xmatch_key_buffer(self.h, max_keys, C.byref(p)))
+        # valid while this XMatch lives (no back reference: no cycle)
+        return _wrap_device_bytes(int(p.value), 8 * max_keys, self.device).view(torch.int64)
+
+    def share_keys(self, key_lo: int, key_hi: int, stream=None) -> None:
+        """Push this rank's hashed shard [key_lo, key_hi) to every peer (copy
+        engine over NVLink); `stream` then waits for every peer's shard."""
+        check(_L.kvx_xmatch_share_keys(self.h, key_lo, key_hi, _stream(stream)))
 
     def run(self, indices: Sequence[BlockIndex], inst_ids: Sequence[int], keys: torch.Tensor,
             key_off: torch.Tensor, out=None, stream=None):

@@ -51,6 +51,8 @@ _sig("kvx_streamer_set_timing", C.c_int, _vp, C.c_int, C.c_int)
 _sig("kvx_streamer_launch_stats", C.c_int, _vp, C.POINTER(_i64), C.POINTER(C.c_double),
      C.POINTER(C.c_double), C.c_int)
 _sig("kvx_streamer_units", C.c_uint64, _vp)
+_sig("kvx_streamer_check", C.c_int, _vp)
+_sig("kvx_streamer_same_gpu", C.c_int, _vp)
 _sig("kvx_streamer_record_begin", C.c_int, _vp)
 _sig("kvx_streamer_record_end", C.c_int, _vp)
 _sig("kvx_streamer_replay", C.c_int, _vp)
@@ -130,6 +132,17 @@ class Streamer:
     def units(self) -> int:
         return int(_L.kvx_streamer_units(self.h))
 
+    def check(self):
+        """Host-blocking: raise if a unit failed since the last check (a pulled
+        unit that timed out waiting for the sender, or out-of-range table
+        entries).  Call after finish() before using the decode slots."""
+        check(_L.kvx_streamer_check(self.h))
+
+    @property
+    def same_gpu(self) -> bool:
+        """The connected peer process shares this GPU (waits are stream ops only)."""
+        return bool(_L.kvx_streamer_same_gpu(self.h))
+
     def record_begin(self):
         """Capture the following sends (local fused mode) into a CUDA graph."""
         check(_L.kvx_streamer_record_begin(self.h))
@@ -204,6 +217,10 @@ class NcclStreamer:
 
     def set_timing(self, on, stride=1):
         pass
+
+    def check(self):
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        torch.cuda.synchronize(self.device)
 
     def launch_stats(self, reset=True):
         return None

@@ -69,3 +69,59 @@ def test_handshake_gloo(world):
         else:
             assert role == "decode" and peer_rank == rank - half and peer_pool is None
         assert peer_tables == [peer_rank * 100 + i for i in range(3)]
+
+
+def test_shard_by_tokens_covers_batch():
+    """Stage-1 request sharding (bench.py --gpus N, "sharded" object): the
+    shards are contiguous, disjoint, cover every request once, and balance
+    tokens to within one request per boundary."""
+    import numpy as np
+
+    from bench import shard_by_tokens
+    rng = np.random.default_rng(3)
+    for world in (1, 2, 3, 4, 8):
+        for n in (0, 1, 5, 4096):
+            lens = rng.integers(0, 24577, size=n)
+            tok_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+            sh = shard_by_tokens(tok_off, world)
+            assert len(sh) == world and sh[0][0] == 0 and sh[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(sh, sh[1:]))
+            assert all(r0 <= r1 for r0, r1 in sh)
+            if n > 100:
+                tot = [int(tok_off[r1] - tok_off[r0]) for r0, r1 in sh]
+                assert max(tot) - min(tot) <= 2 * int(lens.max())
+
+
+def _shard_worker(rank, world, port, q):
+    """Every rank takes its shard; the all-gathered shards rebuild the batch."""
+    import numpy as np
+
+    from bench import shard_by_tokens
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)  # same batch on every rank
+    lens = rng.integers(1, 3000, size=257)
+    tok_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    r0, r1 = shard_by_tokens(tok_off, world)[rank]
+    key_off = np.concatenate([[0], np.cumsum((lens + 15) // 16)])
+    mine = list(range(int(key_off[r0]), int(key_off[r1])))  # key positions this rank hashes
+    out = [None] * world
+    dist.all_gather_object(out, mine)
+    q.put((rank, sorted(k for part in out for k in part) == list(range(int(key_off[-1])))))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_keys_cover_batch_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res)

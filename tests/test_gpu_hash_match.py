@@ -263,3 +263,38 @@ def test_block_hash_concurrent_streams(kvx, oracle_lib):
     torch.cuda.synchronize()
     for i, k in enumerate(outs):
         assert np.array_equal(k.cpu().numpy(), batches[i % 2][2])
+
+
+def test_config4_scale_match_vs_oracle(kvx, oracle_lib):
+    """Config 4 scale: 1M-key instance indices (two instances, Zipf sessions,
+    8K-24K-token requests), the whole batch hashed and matched on the GPU;
+    every per-instance length and every (best_len, best_id) equals the C
+    restatement over the same key sets (kvcache.cpp:150-154,
+    conductor.cpp:57-73)."""
+    from paper_2407_00079_b200.workloads import MatchWorkload
+    mw = MatchWorkload(n_req=1024).build()
+    keys, ko = kvx.chain_hash_batch(_t(mw.tokens, torch.int32), _t(mw.tok_off, torch.int64),
+                                    mw.block_size)
+    wkeys, wko = kvx.chain_hash_batch(_t(mw.warm_tokens, torch.int32),
+                                      _t(mw.warm_tok_off, torch.int64), mw.block_size)
+    wk, wo = wkeys.cpu().numpy(), wko.cpu().numpy()
+    n_sess = len(mw.session_ids)
+    contents = []
+    for inst in range(2):
+        own = np.concatenate([wk[wo[j]:wo[j + 1]] for j in range(n_sess) if j % 2 == inst])
+        own = own[: mw.pool_keys]
+        contents.append(np.concatenate([own, mw.filler_keys(mw.pool_keys - len(own), inst)]))
+    idx = [_index(kvx, c) for c in contents]
+    assert all(ix.stats()["live"] == mw.pool_keys for ix in idx)
+    ids = [7, 2]
+    lens, bl, bi = kvx.match_prefix_batch(idx, ids, keys, ko)
+    k_ref, ko_ref = oracle_lib.block_hash_batch(mw.tokens, mw.tok_off, mw.block_size)
+    assert np.array_equal(keys.cpu().numpy(), k_ref)
+    sets = [oracle_lib.make_set(c) for c in contents]
+    wl, wbl, wbi = oracle_lib.match_prefix_batch(sets, ids, k_ref, ko_ref)
+    for h in sets:
+        oracle_lib.free_set(h)
+    assert wbl.sum() > 0 and (wbl > 0).mean() > 0.5  # the sessions' earlier turns are found
+    assert np.array_equal(lens.cpu().numpy(), wl)
+    assert np.array_equal(bl.cpu().numpy(), wbl)
+    assert np.array_equal(bi.cpu().numpy(), wbi)

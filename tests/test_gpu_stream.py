@@ -120,10 +120,14 @@ def test_streamer_rejects_bad_shapes(kvx):
         Streamer("peer_ce", "sender", src, None, ring=0, slot_bytes=0)
 
 
+_PORT = [29531]
+
+
 def _torchrun(n, *args, timeout=900):
+    _PORT[0] += 1  # a fresh rendezvous port per launch (no TIME_WAIT collisions)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29531", "bench.py", "--gpus", str(n),
-           *args]
+           "--master-addr", "127.0.0.1", "--master-port", str(_PORT[0]), "bench.py", "--gpus",
+           str(n), *args]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1]
@@ -144,3 +148,39 @@ def test_two_gpu_long_context_chunked():
     d = _torchrun(2, "--config", "3", "--block-size", "64", "--steps", "2", "--warmup", "3",
                   "--no-match", "--no-e2e", "--no-cpu-baseline")
     assert d["parity"]["mismatched_words"] == 0 and d["scaling"] == "strong"
+
+
+# ---- the peer protocol on a 1-GPU box: two processes sharing cuda:0 --------
+# Prefill and decode ranks are separate processes (CUDA IPC mappings of the
+# other's pool / ring / flags, gloo handshake) on the same GPU.  No kernel ever
+# waits for the other process there (the pull units are released by stream
+# waits), so the ranks need not run concurrently.  Every destination word is
+# checked by bench.py's verify kernel (a mismatch exits non-zero).
+
+@pytest.mark.parametrize("mode", ["peer_ce", "peer_fused", "peer_pull"])
+def test_shared_gpu_peer_modes_bit_exact(kvx, mode):
+    d = _torchrun(2, "--share-gpu", "--mode", mode, "--requests", "4", "--wave", "2", "--steps",
+                  "2", "--warmup", "3", "--no-match", "--no-e2e", "--no-cpu-baseline",
+                  timeout=600)
+    assert d["parity"]["mismatched_words"] == 0 and d["parity"]["checked_bytes"] > 0
+    assert d["config"]["share_gpu"] and d["config"]["mode"] == mode and d["value"] > 0
+
+
+@pytest.mark.parametrize("mode", ["peer_ce", "peer_pull"])
+def test_shared_gpu_long_context_chunked(kvx, mode):
+    d = _torchrun(2, "--share-gpu", "--mode", mode, "--config", "3", "--block-size", "64",
+                  "--layers-per-chunk", "5", "--steps", "2", "--warmup", "3", "--no-match",
+                  "--no-e2e", "--no-cpu-baseline", timeout=600)
+    assert d["parity"]["mismatched_words"] == 0 and d["scaling"] == "strong"
+    assert d["parity"]["checked_bytes"] == 42949672960  # the whole 128K request, every word
+
+
+def test_shared_gpu_match_exchange(kvx):
+    """Stage 1 at world 2 on one GPU: each process holds one prefill
+    instance; kvx_xmatch combines them in the match kernel (remote atomics into
+    the other process's result buffer + stream flags); rank 0 checks the result
+    against both instances queried together."""
+    d = _torchrun(2, "--share-gpu", "--mode", "peer_ce", "--requests", "2", "--wave", "2",
+                  "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline",
+                  timeout=900)
+    assert d["match"]["config"]["instances"] == 2 and d["match"]["value"] > 0

@@ -21,6 +21,17 @@ def test_xmatch_two_gpus_bit_exact():
     assert r.returncode == 0 and "XMATCH OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+def test_xmatch_shared_gpu_bit_exact(kvx):
+    """The same worker as two processes sharing cuda:0 (gloo handshake): the
+    remote atomics and flags go through CUDA IPC mappings of the other
+    process's buffers on the same device."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29547", "tests/xmatch_worker.py"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "KVX_SHARE_GPU": "1"})
+    assert r.returncode == 0 and "XMATCH OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_xmatch_validation(kvx):
     with pytest.raises(kvx.ValidationError):
         kvx.XMatch(0, 2, 2, 16)  # rank out of range

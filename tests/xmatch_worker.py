@@ -14,9 +14,16 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2407_00079_b200 as pkg  # noqa: E402
 
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-torch.cuda.set_device(rank)
-dist.init_process_group("nccl", device_id=torch.device(f"cuda:{rank}"))
-d = f"cuda:{rank}"
+# KVX_SHARE_GPU=1: every rank on cuda:0 (processes sharing one GPU; gloo
+# handshake) -- the remote atomics and flags then target the same device
+share = os.environ.get("KVX_SHARE_GPU") == "1"
+dev = 0 if share else rank
+torch.cuda.set_device(dev)
+if share:
+    dist.init_process_group("gloo")
+else:
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+d = f"cuda:{dev}"
 rng = np.random.default_rng(5)  # same inputs on every rank
 n_req = 96
 lens = rng.integers(0, 160, n_req)
@@ -34,14 +41,14 @@ def instance_keys(j):
 
 
 def index_of(j):
-    ix = pkg.BlockIndex(rank, 4096)
+    ix = pkg.BlockIndex(dev, 4096)
     ix.insert(instance_keys(j))
     return ix
 
 
 mine = index_of(rank)
 everyone = [index_of(j) for j in range(world)]
-xm = pkg.kvx.XMatch(rank, rank, world, max_req=n_req)
+xm = pkg.kvx.XMatch(dev, rank, world, max_req=n_req)
 blobs = [None] * world
 dist.all_gather_object(blobs, xm.export())
 for b in blobs:
