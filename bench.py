@@ -67,6 +67,8 @@ def parse_args():
     ap.add_argument("--block-size", type=int, default=16)
     ap.add_argument("--dtype-bytes", type=int, default=2)
     ap.add_argument("--no-match", action="store_true")
+    ap.add_argument("--no-tier", action="store_true",
+                    help="skip the DRAM-tier layer-wise load / store line (N=1 only)")
     ap.add_argument("--share-gpu", action="store_true",
                     help="every rank on cuda:0: two processes sharing one GPU run the peer modes' "
                          "IPC + flag protocol and the cross-process match on a 1-GPU box (gloo "
@@ -197,32 +199,114 @@ def ncu_traffic(kernel: str):
 # ---------------------------------------------------------------------------
 # CPU legs (oracle = checker / baseline only)
 
-def cpu_transfer_sample(seconds: float, steps: int = 0, warmup: int = 0):
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def resolve_mode(args, world: int) -> str:
+    mode = args.mode
+    if mode == "auto":
+        # measured best per config (profiles/r01): copy engines for Config 2's
+        # 512 MiB units, the decode GPU pulling for Config 3's 128 MiB units
+        mode = ("local_fused" if world == 1 else
+                "peer_pull" if args.config == 3 else "peer_ce")
+    return mode
+
+
+def layers_per_chunk(args) -> int:
+    return args.layers_per_chunk if args.layers_per_chunk > 0 else (1 if args.config == 2 else 16)
+
+
+def make_workload(args, sample: bool = False):
+    """The config's workload; sample=True: the bounded CPU sample of the same
+    shape (Config 2: 4 requests of 8K tokens with the same 50% shared prefix
+    and decode fragmentation, one decode wave; Config 3: the first 4 chunks)."""
+    from paper_2407_00079_b200.workloads import LongContextWorkload, TransferWorkload
+    kw = dict(block_size=args.block_size, dtype_bytes=args.dtype_bytes)
+    if args.config == 3:
+        return LongContextWorkload(tokens=8192 if sample else 131072, **kw)
+    if args.config == 1:
+        return TransferWorkload(n_req=1, wave=1, **kw)
+    n = min(4, args.requests) if sample else args.requests
+    return TransferWorkload(n_req=n, wave=min(args.wave, n), **kw)
+
+
+def describe_config(args, world: int) -> dict:
+    """The `config` object of both arms (same dict: the driver pairs them)."""
+    from paper_2407_00079_b200.cluster import pair_topology
+    role = pair_topology(world, 0)
+    mode = resolve_mode(args, world)
+    return {**make_workload(args).describe(), "config": args.config, "mode": mode,
+            "copy_impl": args.copy_impl, "layers_per_chunk": layers_per_chunk(args),
+            "cuda_graph": bool(args.graph), "pairs": role.pairs,
+            "share_gpu": bool(args.share_gpu),
+            "parallelism": ("local (prefill+decode on one GPU)" if world == 1 else
+                            f"{role.pairs}P->{role.pairs}D pairs"),
+            "l2": ("inputs far larger than L2 (126 MB); no flush needed" +
+                   ("; inside one layer launch the wave's requests re-read the shared "
+                    "prefix slabs of that layer, which then hit L2 (part of the "
+                    "workload's 50% prefix sharing)" if args.config == 2 else ""))}
+
+
+def cpu_transfer_sample(args, seconds: float, steps: int = 0, warmup: int = 0):
     """The CPU path of the same pipeline (no reference implementation exists:
-    SPEC.md:183): per layer, gather a request's slabs into a buffer and scatter
-    them into the decode pool with memcpy (oracle/kvx_oracle.c), on all host
-    threads.  Sample: one 8K-token request (512 blocks x 80 layers, fp16,
-    bs=16), i.e. 2,684,354,560 payload bytes per pass."""
+    SPEC.md:183): the C restatement's fused paged -> paged copy
+    (oracle/kvx_oracle.c kvo_copy_paged) unit by unit in the bench's order
+    (per decode wave, per layer range), on all host threads, over a bounded
+    sample of the config's workload (make_workload(sample=True)), decode
+    tables from the restated lowest-free allocator."""
     from oracle import Oracle
     o = Oracle()
     threads = os.cpu_count() or 1
-    L, bs, n = 80, 16, 512
-    slab = bs * 8 * 128 * 2
-    src_slots = dst_slots = n
-    src = np.empty(L * 2 * src_slots * slab, dtype=np.uint8)
-    dst = np.empty(L * 2 * dst_slots * slab, dtype=np.uint8)
-    o.fill_pool(src, 0, L, src_slots, slab, nthreads=threads)
-    dst.fill(0)
-    rng = np.random.default_rng(1)
-    st = rng.permutation(src_slots).astype(np.int32)
-    dt = np.arange(n, dtype=np.int32)
-    buf = np.empty(2 * n * slab, dtype=np.uint8)
-    payload = L * 2 * n * slab
+    wl = make_workload(args, sample=True)
+    lpc = layers_per_chunk(args)
+    slab = wl.slab_bytes
+    L = wl.layers
+
+    def lowest_free(slots, pre, n):
+        used = np.zeros(slots, dtype=np.uint8)
+        used[pre] = 1
+        got, t = o.alloc_lowest_free(used, n)
+        assert got == n
+        return t
+
+    if args.config == 3:
+        units_src = [wl.src_table]
+        units_dst = [lowest_free(wl.dst_slots, wl.dst_preoccupied, wl.blocks)]
+        chunk = wl.chunk_blocks
+    else:
+        units_src = [wl.wave_src_table(w) for w in range(wl.n_waves)]
+        units_dst = []
+        for w in range(wl.n_waves):  # every wave from the same fragmented pool (decode_tables)
+            used = np.zeros(wl.dst_slots, dtype=np.uint8)
+            used[wl.dst_preoccupied] = 1
+            tabs = []
+            for _ in wl.wave_requests(w):
+                got, t = o.alloc_lowest_free(used, wl.blocks)
+                assert got == wl.blocks
+                used[t] = 1
+                tabs.append(t)
+            units_dst.append(np.concatenate(tabs))
+        chunk = 0
+    src = np.empty(L * 2 * wl.src_slots * slab, dtype=np.uint8)
+    dst = np.zeros(L * 2 * wl.dst_slots * slab, dtype=np.uint8)
+    o.fill_pool(src, 0, L, wl.src_slots, slab, nthreads=threads)
+    payload = sum(len(t) for t in units_src) * L * 2 * slab
 
     def one_pass():
-        for layer in range(L):
-            o.gather(src, src_slots, slab, st, layer, layer + 1, buf, nthreads=threads)
-            o.scatter(dst, dst_slots, slab, dt, layer, layer + 1, buf, nthreads=threads)
+        for st, dt in zip(units_src, units_dst):
+            cb = chunk or len(st)
+            for b0 in range(0, len(st), cb):
+                for l0 in range(0, L, lpc):
+                    o.copy_paged(src, wl.src_slots, st[b0:b0 + cb], dst, wl.dst_slots,
+                                 dt[b0:b0 + cb], slab, l0, min(L, l0 + lpc), nthreads=threads)
 
     for _ in range(max(warmup, 1)):
         one_pass()
@@ -233,14 +317,18 @@ def cpu_transfer_sample(seconds: float, steps: int = 0, warmup: int = 0):
         t0 = time.perf_counter()
         one_pass()
         times.append(time.perf_counter() - t0)
-    # spot-check the round trip against the generator (parity of the baseline itself)
-    w = dst.view(np.uint64).reshape(L, 2, dst_slots, slab // 8)
-    seed = o.slab_seed(0, 79, 1, int(st[7]))
-    assert int(w[79, 1, 7, 5]) == o.kv_word(seed, 5)
+    # spot-check the copy against the generator (parity of the baseline itself)
+    w = dst.view(np.uint64).reshape(L, 2, wl.dst_slots, slab // 8)
+    seed = o.slab_seed(0, L - 1, 1, int(units_src[-1][7]))
+    assert int(w[L - 1, 1, int(units_dst[-1][7]), 5]) == o.kv_word(seed, 5)
+    what = ("Config 2 sample: 4 requests x 8K tokens, 50% shared prefix, one decode wave"
+            if args.config == 2 else "Config 3 sample: first 4 chunks of the request"
+            if args.config == 3 else "Config 1: one 8K-token request")
     return {"value": payload / statistics.median(times) / GB, "unit": "GB/s", "cores": threads,
-            "kind": "port",
-            "sample": "1 request x 8K tokens (512 blocks x 80 layers x K,V, 2.68 GB payload), "
-                      f"per-layer memcpy gather+scatter, {len(times)} passes, median"}, times
+            "kind": "port", "cpu_model": cpu_model(),
+            "sample": f"{what} ({payload / GB:.2f} GB payload per pass), fused paged->paged "
+                      f"memcpy per ({'chunk, ' if chunk else ''}layer range of {lpc}) unit "
+                      f"(oracle kvo_copy_paged), {len(times)} passes, median"}, times
 
 
 def cpu_match_sample(mw, seconds: float, gpu_len=None, gpu_id=None):
@@ -286,18 +374,21 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    base, times = cpu_transfer_sample(0, steps=args.steps, warmup=args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    base, times = cpu_transfer_sample(args, 0, steps=args.steps, warmup=args.warmup)
     ms = 1e3 * statistics.median(times)
     line = {"impl": "reference",
             "metric": "KVCache layer-wise transfer GB/s (gather+P2P+scatter); prefix-match blocks/s",
             "value": base["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": "config2 shape, CPU sample (see cpu_baseline.sample)",
-                       "parallelism": f"host threads x{base['cores']}"},
+            "config": describe_config(args, world),
             "cpu_baseline": base,
             "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "note": "the reference (kvcsim) has no byte path (SPEC.md:15,183): this arm times "
+                    "the C restatement of the same copy (oracle/kvx_oracle.c) on the host "
+                    "cores; ms_per_step is one pass over the bounded sample"}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -360,12 +451,7 @@ def run_kvx(args):
         if world > 1:
             dist.barrier()
 
-    mode = args.mode
-    if mode == "auto":
-        # measured best per config (profiles/r01): copy engines for Config 2's
-        # 512 MiB units, the decode GPU pulling for Config 3's 128 MiB units
-        mode = ("local_fused" if role.role == "local" else
-                "peer_pull" if args.config == 3 else "peer_ce")
+    mode = resolve_mode(args, world)
     if (role.role == "local") != mode.startswith("local"):
         raise SystemExit(f"mode {mode} does not fit {world} GPU(s)")
     if args.share_gpu and mode == "peer_nccl":
@@ -377,8 +463,7 @@ def run_kvx(args):
         g = probe_link(role, dev)
         link_gbs = -max_over_ranks(-(g if g is not None else 1e30), d)  # slowest pair
 
-    if args.layers_per_chunk <= 0:
-        args.layers_per_chunk = 1 if args.config == 2 else 16
+    args.layers_per_chunk = layers_per_chunk(args)
     plan = build_plan(args, role)
     wl = plan["wl"]
     pool_kw = dict(layers=wl.layers, block_size=wl.block_size, heads=wl.heads,
@@ -563,11 +648,15 @@ def run_kvx(args):
     if not args.no_match:
         match = bench_match(args, dev, rank, world, role)
 
+    tier = None
+    if world == 1 and not args.no_tier:
+        tier = bench_host_tier(args, dev)
+
     torch.cuda.synchronize()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, _ = cpu_transfer_sample(args.cpu_seconds)
+        cpu, _ = cpu_transfer_sample(args, args.cpu_seconds)
 
     peaks = measured_peaks()
     roof = None
@@ -611,17 +700,8 @@ def run_kvx(args):
             "host_wall_ms_per_step": wall_step,
             "dtype": "u8",
             "data": "synthetic (counter-based splitmix64 KV content; generate_workload block ids)",
-            "config": {**plan["describe"], "config": args.config, "mode": mode,
-                       "copy_impl": args.copy_impl, "layers_per_chunk": args.layers_per_chunk,
-                       "cuda_graph": bool(args.graph),
-                       "pairs": role.pairs,
-                       "share_gpu": bool(args.share_gpu),
-                       "parallelism": ("local (prefill+decode on one GPU)" if world == 1 else
-                                       f"{role.pairs}P->{role.pairs}D pairs"),
-                       "l2": ("inputs far larger than L2 (126 MB); no flush needed" +
-                              ("; inside one layer launch the wave's requests re-read the shared "
-                               "prefix slabs of that layer, which then hit L2 (part of the "
-                               "workload's 50% prefix sharing)" if args.config == 2 else ""))},
+            "impl": "kvx",
+            "config": describe_config(args, world),
             "roofline": roof,
             "link": (None if world == 1 or args.share_gpu else {
                 "achieved_per_pair": value / role.pairs, "peak_per_direction": link_gbs,
@@ -635,6 +715,7 @@ def run_kvx(args):
             "parity": {"checked_bytes": checked, "mismatched_words": bad,
                        "check": "verify kernel: every decode slab word == synthetic source word"},
             "match": match,
+            "host_tier": tier,
         }
         print(json.dumps(line), flush=True)
     barrier()
@@ -1036,6 +1117,136 @@ def bench_match_sharded(args, dev, rank, world, s, o):
                                "instances"}}
     del xm
     return out
+
+
+def bench_host_tier(args, dev):
+    """CPU-DRAM tier (a12): one LLaMA2-70B request of 8K tokens whose first
+    half (256 blocks, Config 2's shared prefix) is cached in DRAM.  Measured:
+    the copy-engine PCIe peaks (1 GiB pinned H2D / D2H), the layer-wise load of
+    the prefix DRAM -> HBM and store of the fresh half HBM -> DRAM (copy
+    kernels of host_copy_ctas CTAs over PCIe), and a layer-wise prefill with
+    Mooncake's launch / wait per layer: per layer, wait for the
+    layer's load, run that layer's compute (a bf16 GEMM standing in for the
+    layer: 4096 x 8192 x 8192), launch the layer's store; the reference models
+    it as max(compute, load) (layerwise_effective_prefill,
+    proj/src/perf_model.cpp:73-85)."""
+    import torch
+
+    import paper_2407_00079_b200 as pkg
+    from paper_2407_00079_b200 import kvx
+    d = f"cuda:{dev}"
+    L, bs, n_pre, n_new = 80, args.block_size, 256, 256
+    host_slots = 2048
+    host = pkg.KVPool(L, bs, 8, 128, args.dtype_bytes, host_slots, dev, host=True)
+    hbm = pkg.KVPool(L, bs, 8, 128, args.dtype_bytes, 1024, dev)
+    host.fill_synthetic(7)
+    rng = np.random.default_rng(12)
+    ht = torch.as_tensor(rng.permutation(host_slots)[: n_pre + n_new].astype(np.int32), device=d)
+    dt = torch.as_tensor(rng.permutation(1024)[: n_pre + n_new].astype(np.int32), device=d)
+    h_pre, d_pre = ht[:n_pre], dt[:n_pre]
+    h_new, d_new = ht[n_pre:], dt[n_pre:]
+    slab = hbm.slab
+    load_bytes = L * 2 * n_pre * slab
+    store_bytes = L * 2 * n_new * slab
+    io = kvx.LayerIO(dev, L)
+    s = torch.cuda.Stream(dev)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    # copy-engine PCIe peaks (pinned host memory, 1 GiB, best of 3)
+    nb = 1 << 30
+    pin = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    gbuf = torch.empty(nb, dtype=torch.uint8, device=d)
+
+    def ce(h2d):
+        best = 1e30
+        for _ in range(4):
+            a, b = ev(), ev()
+            a.record(s)
+            with torch.cuda.stream(s):
+                (gbuf.copy_(pin, non_blocking=True) if h2d else pin.copy_(gbuf, non_blocking=True))
+            b.record(s)
+            s.synchronize()
+            best = min(best, a.elapsed_time(b))
+        return nb / (best / 1e3) / GB
+    h2d_peak, d2h_peak = ce(True), ce(False)
+    del pin, gbuf
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(s)
+        for _ in range(reps):
+            fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    def load_all():
+        io.load(host, h_pre, hbm, d_pre, 0, L, after=s)
+        io.wait_layer(L - 1, s)
+
+    def store_all():
+        io.store(hbm, d_new, host, h_new, 0, L, after=s)
+        io.wait_stores(s)
+
+    reps = max(3, min(args.steps, 10))
+    load_ms = timed(load_all, reps)
+    bad = torch.zeros(1, dtype=torch.int64, device=d)
+    hbm.verify(d_pre, 7, h_pre, 0, L, counter=bad, stream=s)
+    s.synchronize()
+    assert bad.item() == 0, "DRAM-tier load parity"
+    with torch.cuda.stream(s):
+        hbm.fill_synthetic(8, stream=s)
+    store_ms = timed(store_all, reps)
+    host.verify(h_new, 8, d_new, 0, L, counter=bad, stream=s)
+    s.synchronize()
+    assert bad.item() == 0, "DRAM-tier store parity"
+
+    # layer-wise prefill: launch / wait per layer around a per-layer GEMM
+    with torch.cuda.stream(s):
+        x = torch.randn(4096, 8192, dtype=torch.bfloat16, device=d)
+        w = torch.randn(8192, 8192, dtype=torch.bfloat16, device=d)
+        y = torch.empty(4096, 8192, dtype=torch.bfloat16, device=d)
+
+    def compute_only():
+        with torch.cuda.stream(s):
+            for _ in range(L):
+                torch.matmul(x, w, out=y)
+
+    def layerwise():
+        io.load(host, h_pre, hbm, d_pre, 0, L, after=s)   # launch every layer's load
+        with torch.cuda.stream(s):
+            for layer in range(L):
+                io.wait_layer(layer, s)                   # wait before the layer's attention
+                torch.matmul(x, w, out=y)
+                io.store(hbm, d_new, host, h_new, layer, layer + 1, after=s)  # launch its store
+        io.wait_stores(s)                                 # all stores at the end
+
+    compute_ms = timed(compute_only, reps)
+    lw_ms = timed(layerwise, reps)
+    return {
+        "metric": "layer-wise DRAM <-> HBM KV load / store GB/s (CPU-DRAM tier)",
+        "workload": "one 8K-token LLaMA2-70B request: 256-block prefix cached in DRAM (load), "
+                    "256 fresh blocks stored back (bs 16, fp16, 80 layers)",
+        "load": {"bytes": load_bytes, "ms": load_ms, "gbs": load_bytes / (load_ms / 1e3) / GB,
+                 "frac_of_h2d_peak": load_bytes / (load_ms / 1e3) / GB / h2d_peak},
+        "store": {"bytes": store_bytes, "ms": store_ms,
+                  "gbs": store_bytes / (store_ms / 1e3) / GB,
+                  "frac_of_d2h_peak": store_bytes / (store_ms / 1e3) / GB / d2h_peak},
+        "pcie_peak": {"h2d_gbs": h2d_peak, "d2h_gbs": d2h_peak,
+                      "how": "copy engine, 1 GiB pinned, best of 4, measured in this run"},
+        "kernel": "copy_lsu_kernel, grid capped for PCIe (KVX_HOST_COPY_CTAS, default 16)",
+        "layerwise_prefill": {
+            "compute_ms": compute_ms, "load_ms": load_ms, "store_ms": store_ms,
+            "measured_ms": lw_ms, "model_ms": max(compute_ms, load_ms),
+            "model": "layerwise_effective_prefill = max(compute, cache load) "
+                     "(proj/src/perf_model.cpp:73-78)",
+            "compute": "per layer one bf16 GEMM 4096x8192x8192 (stand-in for the layer)"},
+        "parity": "every loaded / stored word verified against the synthetic source",
+    }
 
 
 def bench_conductor(args, B, keys, s):

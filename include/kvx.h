@@ -262,6 +262,13 @@ int kvx_pool_verify(const kvx_pool* dst, const int32_t* d_dst_table, uint32_t sr
                     const int32_t* d_src_table, int64_t n, int32_t layer_lo, int32_t layer_hi,
                     uint64_t* d_mismatch, void* stream);
 
+/* CPU-DRAM tier: a pool in pinned, device-mapped host memory (same layout).
+ * desc->device is the GPU whose kernels access it; gather / scatter /
+ * kvx_copy_paged accept it on either side and then run a small grid over
+ * PCIe (zero copy).  Freed by kvx_pool_destroy. */
+int kvx_pool_create_host(const kvx_pool_desc* desc, kvx_pool** out);
+int kvx_pool_is_host(const kvx_pool* pool);
+
 /* ---- stages 2 / 4 / fused ------------------------------------------------ */
 
 int kvx_gather(const kvx_pool* pool, const int32_t* d_src_table, int64_t n, int32_t layer_lo,
@@ -389,6 +396,30 @@ int kvx_streamer_record_begin(kvx_streamer* s);
 int kvx_streamer_record_end(kvx_streamer* s);
 int kvx_streamer_replay(kvx_streamer* s);
 
+/* ---- layer-wise DRAM <-> HBM load / store ---------------
+ * Replaces the reference's cache_load_time / layerwise_effective_prefill
+ * model (proj/src/perf_model.cpp:73-85; load_bandwidth, config.cpp:218) with
+ * the real transfer: "launch" queues a layer's copy on the object's load (or
+ * store) queue, "wait" makes a stream wait for it.  Loads: host pool -> device
+ * pool, one unit per layer in layer order, after the work on after_stream;
+ * kvx_layer_load_wait(layer) before that layer's attention.  Stores: device
+ * pool -> host pool, launched after the work on after_stream (the layer's
+ * attention); kvx_layer_store_wait_all at the end (stream NULL: host-blocking).
+ * Tables are device int32 arrays of n slot ids on each side. */
+typedef struct kvx_layer_io kvx_layer_io;
+int kvx_layer_io_create(int device, int32_t max_layers, kvx_layer_io** out);
+int kvx_layer_io_destroy(kvx_layer_io* io);
+void* kvx_layer_io_load_stream(kvx_layer_io* io);
+void* kvx_layer_io_store_stream(kvx_layer_io* io);
+int kvx_layer_load_launch(kvx_layer_io* io, const kvx_pool* host, const int32_t* d_host_table,
+                          kvx_pool* dev, const int32_t* d_dev_table, int64_t n, int32_t layer_lo,
+                          int32_t layer_hi, void* after_stream);
+int kvx_layer_load_wait(kvx_layer_io* io, int32_t layer, void* stream);
+int kvx_layer_store_launch(kvx_layer_io* io, const kvx_pool* dev, const int32_t* d_dev_table,
+                           kvx_pool* host, const int32_t* d_host_table, int64_t n,
+                           int32_t layer_lo, int32_t layer_hi, void* after_stream);
+int kvx_layer_store_wait_all(kvx_layer_io* io, void* stream);
+
 /* ---- KVCache store of one instance + migration (hot-spot replication) ---- */
 
 /* A store = paged pool + block index (key -> pool slot) + slot allocator.
@@ -399,7 +430,8 @@ int kvx_streamer_replay(kvx_streamer* s);
  * behind the reference's migration events (sim_engine.cpp:399-419,605-650).
  * If ANY key is not resident in src the call returns KVX_EABORTED and changes
  * nothing (the reference aborts when the source evicted part of the range).
- * All key/slot arrays are HOST arrays; calls are host-blocking. */
+ * All key/slot arrays are HOST arrays; put / get / evict / migrate are
+ * host-blocking. */
 typedef struct kvx_store kvx_store;
 int kvx_store_create(const kvx_pool_desc* desc, kvx_store** out);
 int kvx_store_destroy(kvx_store* s);
@@ -411,6 +443,30 @@ int kvx_store_get(kvx_store* s, const int64_t* keys, int64_t n, int32_t* slots_o
 int kvx_store_evict(kvx_store* s, const int64_t* keys, int64_t n);
 int kvx_store_migrate(kvx_store* src, kvx_store* dst, const int64_t* keys, int64_t n,
                       int64_t* n_copied);
+/* Asynchronous migration, engine-driven (sim_engine.cpp:399-419,605-650).
+ * Each SOURCE store has one in-order migration FIFO (the per-sender link,
+ * sender_busy_until_ms, sim_engine.cpp:409-411).  submit queues the
+ * migration (keys copied to the host-side FIFO) and returns a ticket; it
+ * BEGINS when it reaches the head of the FIFO and the previous migration is
+ * done: then the source is checked (any key not resident -> the ticket ends
+ * KVX_EABORTED and nothing lands), destination slots are reserved and the copy
+ * is launched after the work queued on the source store's stream and, if
+ * after_stream != NULL, on after_stream at submit time.  Source slots stay
+ * pinned until the copy is done (an eviction meanwhile drops the key but
+ * defers the slot's reuse).  It is DONE when the copy finished: the keys land
+ * in the destination index (blocks that became resident there meanwhile are
+ * kept and the copied slot is freed).  Progress happens inside submit /
+ * query / wait / progress calls on the source store (no threads):
+ *   query: KVX_OK done, KVX_EAGAIN in flight or queued, KVX_EABORTED aborted;
+ *   wait:  host-blocking until done; *n_copied = blocks landed; collects the
+ *          ticket (a later query/wait of it is KVX_EINVAL).
+ * kvx_store_migrate = submit + wait.  Destroy stores only after their
+ * migrations are collected. */
+int kvx_store_migrate_submit(kvx_store* src, kvx_store* dst, const int64_t* keys, int64_t n,
+                             void* after_stream, uint64_t* ticket);
+int kvx_store_migrate_query(kvx_store* src, uint64_t ticket);
+int kvx_store_migrate_wait(kvx_store* src, uint64_t ticket, int64_t* n_copied);
+int kvx_store_migrate_progress(kvx_store* src);
 
 /* ---- decode block table: deterministic slot allocator (host) ---------- */
 

@@ -33,6 +33,18 @@ namespace {
 
 int g_copy_impl = 0;
 
+// CTAs of a copy that crosses PCIe (a host pool on either side).  16 CTAs x
+// 512 threads x 8 x 16 B in flight = 1 MiB outstanding, well above the
+// PCIe bandwidth-delay product; KVX_HOST_COPY_CTAS overrides (measurement).
+int host_copy_ctas() {
+  static const int v = [] {
+    const char* e = std::getenv("KVX_HOST_COPY_CTAS");
+    const int x = e ? std::atoi(e) : 16;
+    return x >= 1 ? x : 16;
+  }();
+  return v;
+}
+
 struct SlabCopy {
   const uint8_t* src;
   uint8_t* dst;
@@ -391,11 +403,14 @@ int launch_tma(const SlabCopy& c, int dev, int ctas_per_sm, cudaStream_t s) {
 // overlap_prev: launch with programmatic stream serialization (the copy may
 // start while the previous kernel on the stream runs; caller guarantees the
 // two touch disjoint bytes).  LSU copy only.
-int launch_copy(const SlabCopy& c, int dev, cudaStream_t s, bool overlap_prev = false) {
+// max_ctas > 0 caps the grid (copies that cross PCIe: a few CTAs keep the link
+// busy and leave the other SMs to compute).
+int launch_copy(const SlabCopy& c, int dev, cudaStream_t s, bool overlap_prev = false,
+                int max_ctas = 0) {
   const int64_t units = c.planes * c.n;
   if (units == 0 || c.slab == 0) return KVX_OK;
   const int sms = sm_count(dev);
-  if (g_copy_impl == 1) {
+  if (g_copy_impl == 1 && max_ctas == 0) {
     static const int cfg = [] {
       const char* e = std::getenv("KVX_TMA_CFG");  // tuning knob
       return e ? std::atoi(e) : 0;
@@ -418,8 +433,9 @@ int launch_copy(const SlabCopy& c, int dev, cudaStream_t s, bool overlap_prev = 
       return v >= 1 && v <= 4 ? v : 4;
     }();
     const int64_t items = units * ((c.slab + kLsuItem - 1) / kLsuItem);
-    const int blocks =
-        static_cast<int>(std::min<int64_t>(items, static_cast<int64_t>(sms) * ctas_per_sm));
+    int64_t cap = static_cast<int64_t>(sms) * ctas_per_sm;
+    if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
+    const int blocks = static_cast<int>(std::min<int64_t>(items, cap));
     static const int variant = [] {
       const char* e = std::getenv("KVX_LSU_VARIANT");  // measurement knob
       return e ? std::atoi(e) : 0;
@@ -516,6 +532,7 @@ struct kvx_pool {
   int64_t bytes = 0;
   uint8_t* base = nullptr;
   bool owned = false;
+  bool host = false;  // pinned, device-mapped CPU DRAM (the KVCache DRAM tier)
 };
 
 namespace {
@@ -609,9 +626,36 @@ int kvx_pool_create_view(const kvx_pool_desc* desc, void* d_base, kvx_pool** out
   return KVX_OK;
 }
 
+int kvx_pool_create_host(const kvx_pool_desc* desc, kvx_pool** out) {
+  int st = check_desc(desc);
+  if (st) return st;
+  KVX_REQUIRE(out != nullptr, "kvx_pool_create_host: out is NULL");
+  DeviceGuard g(desc->device);
+  auto* p = new kvx_pool();
+  p->d = *desc;
+  p->slab = static_cast<int64_t>(desc->block_size) * desc->heads * desc->head_dim * desc->dtype_bytes;
+  p->bytes = static_cast<int64_t>(desc->layers) * 2 * desc->slots * p->slab;
+  // pinned + mapped: kernels on any GPU address it directly (UVA: the host
+  // pointer is the device pointer), reads and writes cross PCIe
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p->base), static_cast<size_t>(p->bytes),
+                                cudaHostAllocPortable | cudaHostAllocMapped);
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_error(e, "kvx_pool_create_host: cudaHostAlloc");
+  }
+  p->owned = true;
+  p->host = true;
+  *out = p;
+  return KVX_OK;
+}
+
+int kvx_pool_is_host(const kvx_pool* p) { return p && p->host ? 1 : 0; }
+
 int kvx_pool_destroy(kvx_pool* p) {
   if (!p) return KVX_OK;
-  if (p->owned && p->base) {
+  if (p->owned && p->base && p->host) {
+    cudaFreeHost(p->base);
+  } else if (p->owned && p->base) {
     DeviceGuard g(p->d.device);
     cudaFree(p->base);
   }
@@ -680,7 +724,7 @@ int kvx_gather(const kvx_pool* p, const int32_t* d_src_table, int64_t n, int32_t
   c.planes = static_cast<int64_t>(hi - lo) * 2;
   c.slab = p->slab;
   DeviceGuard g(p->d.device);
-  return launch_copy(c, p->d.device, as_stream(stream));
+  return launch_copy(c, p->d.device, as_stream(stream), false, p->host ? host_copy_ctas() : 0);
 }
 
 int kvx_scatter(kvx_pool* p, const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi,
@@ -704,7 +748,7 @@ int kvx_scatter(kvx_pool* p, const int32_t* d_dst_table, int64_t n, int32_t lo, 
   c.planes = static_cast<int64_t>(hi - lo) * 2;
   c.slab = p->slab;
   DeviceGuard g(p->d.device);
-  return launch_copy(c, p->d.device, as_stream(stream));
+  return launch_copy(c, p->d.device, as_stream(stream), false, p->host ? host_copy_ctas() : 0);
 }
 
 int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
@@ -713,8 +757,12 @@ int kvx_copy_paged(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* ds
   bool empty = false;
   const int st = kvx::paged_copy_args(src, d_src_table, dst, d_dst_table, n, lo, hi, &c, &empty);
   if (st || empty) return st;
-  DeviceGuard g(src->d.device);
-  return launch_copy(c, src->d.device, as_stream(stream));
+  // the kernel runs on the device of the stream's pools: a host (DRAM-tier)
+  // pool is accessed by the GPU of the other side
+  const int dev = src->host ? dst->d.device : src->d.device;
+  DeviceGuard g(dev);
+  return launch_copy(c, dev, as_stream(stream), false,
+                     (src->host || dst->host) ? host_copy_ctas() : 0);
 }
 
 }  // extern "C"

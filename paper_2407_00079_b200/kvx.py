@@ -115,6 +115,16 @@ _sig("kvx_xmatch_run", C.c_int, _vp, C.POINTER(_vp), C.POINTER(_i32), _i64, _vp,
      _vp, _vp)
 _sig("kvx_pool_create", C.c_int, C.POINTER(KvxPoolDesc), C.POINTER(_vp))
 _sig("kvx_pool_create_view", C.c_int, C.POINTER(KvxPoolDesc), _vp, C.POINTER(_vp))
+_sig("kvx_pool_create_host", C.c_int, C.POINTER(KvxPoolDesc), C.POINTER(_vp))
+_sig("kvx_pool_is_host", C.c_int, _vp)
+_sig("kvx_layer_io_create", C.c_int, C.c_int, C.c_int32, C.POINTER(_vp))
+_sig("kvx_layer_io_destroy", C.c_int, _vp)
+_sig("kvx_layer_io_load_stream", _vp, _vp)
+_sig("kvx_layer_io_store_stream", _vp, _vp)
+_sig("kvx_layer_load_launch", C.c_int, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp)
+_sig("kvx_layer_load_wait", C.c_int, _vp, _i32, _vp)
+_sig("kvx_layer_store_launch", C.c_int, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp)
+_sig("kvx_layer_store_wait_all", C.c_int, _vp, _vp)
 _sig("kvx_pool_destroy", C.c_int, _vp)
 _sig("kvx_pool_base", _vp, _vp)
 _sig("kvx_pool_slab_bytes", _i64, _vp)
@@ -413,10 +423,15 @@ class KVPool:
     """Paged KV pool: HBM layout [layer][K|V][slot][block_size][heads][head_dim]."""
 
     def __init__(self, layers: int, block_size: int, heads: int, head_dim: int, dtype_bytes: int,
-                 slots: int, device: int = 0, base_ptr: Optional[int] = None):
+                 slots: int, device: int = 0, base_ptr: Optional[int] = None, host: bool = False):
+        """host=True: the CPU-DRAM tier (pinned, device-mapped host memory, same
+        layout), accessed by GPU `device`'s copy kernels over PCIe."""
         self.desc = KvxPoolDesc(layers, block_size, heads, head_dim, dtype_bytes, slots, device)
         h = _vp()
-        if base_ptr is None:
+        self.host = host
+        if host:
+            check(_L.kvx_pool_create_host(C.byref(self.desc), C.byref(h)))
+        elif base_ptr is None:
             check(_L.kvx_pool_create(C.byref(self.desc), C.byref(h)))
         else:
             check(_L.kvx_pool_create_view(C.byref(self.desc), _vp(base_ptr), C.byref(h)))
@@ -466,6 +481,12 @@ class KVPool:
         assert src_table.numel() == dst_table.numel()
         check(_L.kvx_copy_paged(self.h, _ptr(src_table), dst.h, _ptr(dst_table),
                                 src_table.numel(), layer_lo, layer_hi, _stream(stream)))
+
+    def host_array(self):
+        """numpy uint8 view of a host (DRAM-tier) pool's bytes (no copy)."""
+        import numpy as np
+        assert self.host, "host_array: not a host pool"
+        return np.ctypeslib.as_array((C.c_uint8 * self.nbytes).from_address(self.base))
 
     def tensor_view(self) -> torch.Tensor:
         """uint8 torch view of the whole pool (tests only; does not own memory)."""
@@ -549,6 +570,50 @@ def signal_write(flag_ptr: int, value: int, stream=None) -> None:
 
 def signal_wait(flag_ptr: int, value: int, stream=None) -> None:
     check(_L.kvx_signal_wait(_vp(_stream(stream)), _vp(flag_ptr), value))
+
+
+class LayerIO:
+    """Layer-wise DRAM <-> HBM KV load / store with launch / wait per layer
+    (the reference's cache_load_time / layerwise_effective_prefill,
+    proj/src/perf_model.cpp:73-85)."""
+
+    def __init__(self, device: int, max_layers: int):
+        h = _vp()
+        check(_L.kvx_layer_io_create(device, max_layers, C.byref(h)))
+        self.h, self.device = h, device
+        self.load_stream = torch.cuda.ExternalStream(int(_L.kvx_layer_io_load_stream(h)),
+                                                     device=device)
+        self.store_stream = torch.cuda.ExternalStream(int(_L.kvx_layer_io_store_stream(h)),
+                                                      device=device)
+
+    def close(self):
+        if getattr(self, "h", None) and _ALIVE is True:
+            _L.kvx_layer_io_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def load(self, host: "KVPool", host_table: torch.Tensor, dev: "KVPool",
+             dev_table: torch.Tensor, layer_lo: int, layer_hi: int, after=None):
+        assert host_table.numel() == dev_table.numel()
+        check(_L.kvx_layer_load_launch(self.h, host.h, _ptr(host_table), dev.h, _ptr(dev_table),
+                                       dev_table.numel(), layer_lo, layer_hi,
+                                       _stream(after) if after is not None else None))
+
+    def wait_layer(self, layer: int, stream=None):
+        check(_L.kvx_layer_load_wait(self.h, layer, _stream(stream)))
+
+    def store(self, dev: "KVPool", dev_table: torch.Tensor, host: "KVPool",
+              host_table: torch.Tensor, layer_lo: int, layer_hi: int, after=None):
+        assert host_table.numel() == dev_table.numel()
+        check(_L.kvx_layer_store_launch(self.h, dev.h, _ptr(dev_table), host.h, _ptr(host_table),
+                                        dev_table.numel(), layer_lo, layer_hi,
+                                        _stream(after) if after is not None else None))
+
+    def wait_stores(self, stream=None):
+        """stream None: host-blocking."""
+        check(_L.kvx_layer_store_wait_all(self.h, _stream(stream) if stream is not None
+                                          else None))
 
 
 class DeviceBuffer:

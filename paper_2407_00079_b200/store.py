@@ -32,6 +32,10 @@ _sig("kvx_store_put", C.c_int, _vp, _i64p, _i64, _i32p)
 _sig("kvx_store_get", C.c_int, _vp, _i64p, _i64, _i32p)
 _sig("kvx_store_evict", C.c_int, _vp, _i64p, _i64)
 _sig("kvx_store_migrate", C.c_int, _vp, _vp, _i64p, _i64, C.POINTER(_i64))
+_sig("kvx_store_migrate_submit", C.c_int, _vp, _vp, _i64p, _i64, _vp, C.POINTER(C.c_uint64))
+_sig("kvx_store_migrate_query", C.c_int, _vp, C.c_uint64)
+_sig("kvx_store_migrate_wait", C.c_int, _vp, C.c_uint64, C.POINTER(_i64))
+_sig("kvx_store_migrate_progress", C.c_int, _vp)
 
 
 class KVStore:
@@ -84,3 +88,35 @@ class KVStore:
         n = _i64()
         check(_L.kvx_store_migrate(self.h, dst.h, k.ctypes.data_as(_i64p), len(k), C.byref(n)))
         return n.value
+
+    def migrate_submit(self, dst: "KVStore", keys, after_stream=None) -> int:
+        """Queue a migration of `keys` to dst on this store's sender FIFO;
+        returns a ticket.  It begins (residency check, copy launch) when the
+        earlier migrations of this sender are done (sim_engine.cpp:409-411)."""
+        k = np.ascontiguousarray(keys, dtype=np.int64)
+        t = C.c_uint64()
+        check(_L.kvx_store_migrate_submit(
+            self.h, dst.h, k.ctypes.data_as(_i64p), len(k),
+            kvx._stream(after_stream) if after_stream is not None else None, C.byref(t)))
+        return t.value
+
+    def migrate_query(self, ticket: int) -> str:
+        """'done' | 'pending' | 'aborted' (never blocks)."""
+        rc = _L.kvx_store_migrate_query(self.h, ticket)
+        if rc == kvx.KVX_EAGAIN:
+            return "pending"
+        if rc == kvx.KVX_EABORTED:
+            return "aborted"
+        check(rc)
+        return "done"
+
+    def migrate_wait(self, ticket: int) -> int:
+        """Block until the migration is done; returns the blocks that landed.
+        Raises TransferAborted if the source evicted part of the range before
+        the migration began."""
+        n = _i64()
+        check(_L.kvx_store_migrate_wait(self.h, ticket, C.byref(n)))
+        return n.value
+
+    def migrate_progress(self) -> None:
+        check(_L.kvx_store_migrate_progress(self.h))

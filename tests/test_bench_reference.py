@@ -24,3 +24,8 @@ def test_reference_arm_json_line():
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == line["value"]
     assert line["e2e"] == {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
+    # the same config object as the kvx arm at N=1 (the driver pairs the two lines)
+    cfg = line["config"]
+    assert cfg["workload"].startswith("config2") and cfg["mode"] == "local_fused"
+    assert cfg["requests"] == 64 and cfg["layers_per_chunk"] == 1
+    assert "Config 2 sample" in cb["sample"] and cb["cpu_model"]

@@ -91,3 +91,71 @@ def test_repeated_keys_take_one_slot(stores):
     assert b.get([11, 12]).tolist() == [0, 1]
     ctr = b.pool.verify(_t([0, 1]), 7, _t(a_slots), 0, 4)
     assert ctr.item() == 0
+
+
+# ---- asynchronous, engine-driven migration (kvx_store_migrate_submit/wait) ----
+# The reference engine's two migration KATs (proj/tests/test_engine.cpp:170-231)
+# replayed with real bytes: a per-sender FIFO of transfers
+# (sim_engine.cpp:409-411), the residency check at BEGIN (:605-639) and the
+# landing at DONE (:641-650).
+
+def test_async_migration_replicates_prefix(kvx):
+    """test_engine.cpp:170-189: instance 0 holds the chain {1,2,3,4}; the
+    migration replicates it onto instance 1 with the bytes; afterwards the
+    whole prefix is reusable there, so replicating it again copies nothing."""
+    from paper_2407_00079_b200.store import KVStore
+    a = KVStore(4, 16, 8, 128, 2, 8, 0)
+    b = KVStore(4, 16, 8, 128, 2, 8, 0)
+    a.pool.fill_synthetic(3)
+    chain = [1, 2, 3, 4]
+    a_slots = a.put(chain)
+    t = a.migrate_submit(b, chain)
+    assert a.migrate_wait(t) == 4
+    b_slots = b.get(chain)
+    assert (b_slots >= 0).all()
+    assert b.pool.verify(_t(b_slots), 3, _t(a_slots), 0, 4).item() == 0
+    t2 = a.migrate_submit(b, chain)  # replication growth: already resident at b
+    assert a.migrate_wait(t2) == 0
+    assert np.array_equal(b.get(chain), b_slots)
+
+
+def test_async_migration_fifo_abort(kvx):
+    """test_engine.cpp:191-231: two migrations of the hot prefix {1,2,3,4}
+    queue on instance 0's sender FIFO; a fresh chain {11,...,14} arriving at
+    instance 0 evicts the hot blocks before the SECOND begins.  The first
+    (already begun) completes with the right bytes, the second aborts and
+    lands nothing: migrations_completed == 1, migrations_aborted == 1.  The
+    evicted slots the first copy still reads are not handed to the fresh
+    chain until that copy is done."""
+    from paper_2407_00079_b200.kvx import TransferAborted
+    from paper_2407_00079_b200.store import KVStore
+    L = 4
+    a = KVStore(L, 16, 8, 128, 2, 8, 0)
+    b = KVStore(L, 16, 8, 128, 2, 16, 0)
+    other = kvx.KVPool(L, 16, 8, 128, 2, 8, 0)
+    a.pool.fill_synthetic(3)
+    other.fill_synthetic(9)
+    torch.cuda.synchronize()
+    hot = [1, 2, 3, 4]
+    a_slots = a.put(hot)
+    gate = torch.cuda.Stream(0)  # holds the first transfer on the link (~0.2 s)
+    with torch.cuda.stream(gate):
+        torch.cuda._sleep(400_000_000)
+    t1 = a.migrate_submit(b, hot, after_stream=gate)  # begins now, copy behind the gate
+    t2 = a.migrate_submit(b, hot)                     # queued behind t1 on the FIFO
+    assert a.migrate_query(t1) == "pending" and a.migrate_query(t2) == "pending"
+    # r3 at instance 0: the hot blocks are evicted, the fresh chain's KV is written
+    a.evict(hot)
+    fresh = a.put([11, 12, 13, 14])
+    assert not set(fresh.tolist()) & set(a_slots.tolist())  # pinned slots not reused yet
+    other.copy_to(a.pool, _t(np.arange(4)), _t(fresh), 0, L)  # r3's prefill writes its KV
+    assert a.migrate_wait(t1) == 4
+    b_slots = b.get(hot)
+    assert b.pool.verify(_t(b_slots), 3, _t(a_slots), 0, L).item() == 0  # the hot KV, intact
+    with pytest.raises(TransferAborted):
+        a.migrate_wait(t2)
+    assert np.array_equal(b.get(hot), b_slots)  # the aborted one landed nothing
+    # the deferred slots are free again once the first copy is done
+    assert sorted(a.put([100, 101, 102, 103]).tolist()) == sorted(a_slots.tolist())
+    with pytest.raises(kvx.ValidationError):
+        a.migrate_wait(t1)  # collected

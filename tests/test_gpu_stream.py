@@ -176,11 +176,18 @@ def test_shared_gpu_long_context_chunked(kvx, mode):
 
 
 def test_shared_gpu_match_exchange(kvx):
-    """Stage 1 at world 2 on one GPU: each process holds one prefill
-    instance; kvx_xmatch combines them in the match kernel (remote atomics into
-    the other process's result buffer + stream flags); rank 0 checks the result
-    against both instances queried together."""
+    """Stage 1 at world 2 on one GPU.  Headline: each process its own batch
+    against its own 1M-key index, every (best_len, best_id) checked against
+    the oracle.  "sharded": ONE batch, each process hashes its shard of the
+    requests and pushes the keys into the other's key buffer
+    (kvx_xmatch_share_keys), each holds one prefill instance and kvx_xmatch
+    combines them in the match kernel (remote atomics + stream flags); the
+    keys and the global best are checked against the oracle."""
     d = _torchrun(2, "--share-gpu", "--mode", "peer_ce", "--requests", "2", "--wave", "2",
                   "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline",
                   timeout=900)
-    assert d["match"]["config"]["instances"] == 2 and d["match"]["value"] > 0
+    m = d["match"]
+    assert m["value"] > 0 and m["scaling"] == "weak"
+    assert m["parity"]["best_match"]["requests"] == 2 * 4096
+    assert m["parity"]["best_match"]["mismatched"] == 0
+    assert m["sharded"]["parity"]["mismatched"] == 0 and m["sharded"]["value"] > 0
