@@ -10,6 +10,7 @@ from .kvx import (  # noqa: F401
     BlockIndex,
     KVPool,
     KvxError,
+    LayerIO,
     TransferEngine,
     ValidationError,
     XMatch,

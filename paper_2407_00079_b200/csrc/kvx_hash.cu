@@ -338,16 +338,24 @@ struct Cursor {
 
 // Claim requests (index into the longest-first order) until a non-empty one
 // or the batch is exhausted.  Called by all 32 lanes; halves claim independently.
+// `first` (uniform over the half): a pre-assigned first claim, or ~0 -- then
+// the shared counter hands out indices from `base` on.
 __device__ __forceinline__ void claim(Cursor& c, bool need, int hl, int j, int bs,
                                       const int32_t* __restrict__ tokens,
                                       const int64_t* __restrict__ tok_off,
                                       const int64_t* __restrict__ key_off, int64_t n_req,
                                       const int32_t* __restrict__ order,
-                                      unsigned long long* ctr) {
+                                      unsigned long long* ctr, unsigned long long& first,
+                                      unsigned long long base) {
   while (__any_sync(0xffffffffu, need)) {
     unsigned long long idx = 0;
-    if (need && hl == 0) idx = atomicAdd(ctr, 1ull);
-    idx = __shfl_sync(0xffffffffu, idx, 0, 16);
+    if (need && first != ~0ull) {
+      idx = first;
+      first = ~0ull;
+    } else {
+      if (need && hl == 0) idx = base + atomicAdd(ctr, 1ull);
+      idx = __shfl_sync(0xffffffffu, idx, 0, 16);
+    }
     if (need) {
       if (idx >= static_cast<unsigned long long>(n_req)) {
         c.live = false;
@@ -471,7 +479,7 @@ template <int V>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
     int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
-    const int32_t* __restrict__ order, unsigned long long* ctr) {
+    const int32_t* __restrict__ order, unsigned long long* ctr, int prio) {
   extern __shared__ __align__(16) unsigned char hw_smem_raw[];
   WarpSmem<V>& S = reinterpret_cast<WarpSmem<V>*>(hw_smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -485,6 +493,22 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
   // one): wait for its order / counter before reading anything
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
+  // First claims by warp priority: the warp scheduler issues the highest
+  // ready warp id first, so the highest warp of every SM sub-partition takes
+  // the longest requests (their key chains set the batch time and then run
+  // at their dependency latency), the next warps the next longest; later
+  // claims come from the shared counter, longest first.  prio == 0: every
+  // claim from the counter (the r01 behaviour).
+  const int nwarps = static_cast<int>(blockDim.x >> 5), warp = static_cast<int>(threadIdx.x >> 5);
+  const unsigned long long halves = 2ull * V * nwarps * gridDim.x;
+  unsigned long long first[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v)
+    first[v] = prio ? ((static_cast<unsigned long long>(nwarps - 1 - warp) * gridDim.x +
+                        blockIdx.x) * 2 + half) * V + v
+                    : ~0ull;
+  const unsigned long long base = prio ? halves : 0ull;
+
   Cursor P[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) {
@@ -492,7 +516,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
     P[v].a = tokens;
     P[v].prem = P[v].ntok = P[v].nblk = P[v].k = P[v].u = P[v].m = 0;
     P[v].kb0 = 0;
-    claim(P[v], true, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr);
+    claim(P[v], true, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first[v], base);
   }
 #pragma unroll 1
   for (int i = 0; i < kPrefetch; ++i) {
@@ -500,7 +524,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
     for (int v = 0; v < V; ++v) {
       issue(P[v], S.h[v][half], i, hl, j, bs, nsub, tokens);
       claim(P[v], step_cursor(P[v], bs, nsub), hl, j, bs, tokens, tok_off, key_off, n_req, order,
-            ctr);
+            ctr, first[v], base);
     }
   }
 
@@ -520,7 +544,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
     for (int v = 0; v < V; ++v) {
       issue(P[v], S.h[v][half], (it + kPrefetch) % kSlots, hl, j, bs, nsub, tokens);
       claim(P[v], step_cursor(P[v], bs, nsub), hl, j, bs, tokens, tok_off, key_off, n_req, order,
-            ctr);
+            ctr, first[v], base);
     }
     // V commit groups per sub-round: wait until only kPrefetch sub-rounds are pending
     asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch * V) : "memory");
@@ -779,8 +803,13 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
     cfg.numAttrs = (order && pdl) ? 1 : 0;  // PDL only behind our own order kernel
     const int bsi = static_cast<int>(bs);
     unsigned long long* ctr = ws + 1;
+    static const int prio = [] {
+      const char* e = std::getenv("KVX_HASH_PRIO");  // measurement knob: 0 = counter-only claims
+      return e ? std::atoi(e) : 1;
+    }();
     KVX_CUDA(cudaLaunchKernelEx(&cfg, hw::halfwarp_hash_kernel<1>, d_tokens, d_tok_off, n_req,
-                                bsi, d_key_off, d_keys, static_cast<const int32_t*>(order), ctr));
+                                bsi, d_key_off, d_keys, static_cast<const int32_t*>(order), ctr,
+                                order ? prio : 0));
     KVX_LAUNCH_CHECK("halfwarp_hash_kernel");
     return KVX_OK;
   }

@@ -24,5 +24,11 @@ for _ in range(10):
     pkg.chain_hash_batch(tokens, tok_off, 16, key_off=key_off, keys=keys)
 e1.record()
 torch.cuda.synchronize()
+ok = "n/a"
+if os.environ.get("KVX_HASH_FOLD_SMS") != "-1":  # keys are final: check them all
+    from oracle import Oracle
+    want, _ = Oracle().block_hash_batch(mw.tokens, mw.tok_off, 16)
+    ok = bool((keys.cpu().numpy() == want).all())
 print(f"fold_sms={os.environ.get('KVX_HASH_FOLD_SMS', 'auto')} "
-      f"hash batch: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us")
+      f"prio={os.environ.get('KVX_HASH_PRIO', '1')} warps={os.environ.get('KVX_HASH_HW_WARPS', '12')} "
+      f"hash batch: {e0.elapsed_time(e1) / 10 * 1e3:.1f} us parity={ok}")

@@ -69,10 +69,11 @@ def nvlink_counters():
         if ln.startswith("GPU "):
             gpu = int(ln.split()[1].rstrip(":"))
             out[gpu] = {"tx_kib": 0, "rx_kib": 0}
-        elif gpu is not None and "Data Tx" in ln:
-            out[gpu]["tx_kib"] += int(ln.split(":")[-1].strip().split()[0])
-        elif gpu is not None and "Data Rx" in ln:
-            out[gpu]["rx_kib"] += int(ln.split(":")[-1].strip().split()[0])
+        elif gpu is not None and ("Data Tx" in ln or "Data Rx" in ln):
+            v = ln.split(":")[-1].strip().split()[0]
+            if not v.isdigit():  # "N/A": this driver exposes no throughput counters
+                return None
+            out[gpu]["tx_kib" if "Data Tx" in ln else "rx_kib"] += int(v)
     return out
 
 
