@@ -106,6 +106,18 @@ int kvx_index_device(const kvx_index* idx);
 int kvx_index_insert(kvx_index* idx, const int64_t* d_keys, const int64_t* d_values, int64_t n,
                      void* stream);
 int kvx_index_erase(kvx_index* idx, const int64_t* d_keys, int64_t n, void* stream);
+/* Erase d_erase[0..ne) and upsert d_insert[0..ni) (values d_values, or the
+ * position when NULL) in ONE kernel launch.  The two key sets must be
+ * disjoint (the block manager's put: its victims and its new blocks). */
+int kvx_index_update(kvx_index* idx, const int64_t* d_erase, int64_t ne, const int64_t* d_insert,
+                     const int64_t* d_values, int64_t ni, void* stream);
+/* Keep this index's key array resident in L2 for kernels launched on
+ * `stream` (a persisting access-policy window over the table, sized to the
+ * device's persisting-L2 carve-out, which this call raises if needed): the
+ * prefix match probes it at random right after the hash streams the batch's
+ * tokens.  on == 0 removes the stream's window.  The rebuilt table of a
+ * later resize is not covered: call again after large inserts. */
+int kvx_index_l2_pin(const kvx_index* idx, void* stream, int on);
 /* d_values_out[i] = value of key i, or -1 when absent. */
 int kvx_index_lookup(const kvx_index* idx, const int64_t* d_keys, int64_t n,
                      int64_t* d_values_out, void* stream);
@@ -497,6 +509,20 @@ int kvx_enable_peer(int device, int peer_device);
 /* Stream-ordered flag store / wait (no kernel spins: the stream front end
  * waits).  wait: proceeds once *(uint64*)d_flag >= value. */
 int kvx_signal_write(void* stream, void* d_flag, uint64_t value);
+
+/* Plumbing for C / C++ hosts that have no CUDA runtime of their own (the
+ * drop-in libkvcsim_gpu.so calls only these and the entry points above):
+ * a non-blocking stream; pinned, device-mapped host memory (kernels may read
+ * and write it directly, e.g. query keys in and results out); an async copy;
+ * a host-blocking wait until a pinned word the GPU writes reaches `target`
+ * (signed >=; polling, no synchronise call; errors of `stream` and a stream
+ * that went idle without writing are reported). */
+int kvx_stream_create(int device, void** stream_out);
+int kvx_stream_destroy(void* stream);
+int kvx_host_alloc(int64_t bytes, void** host_ptr);
+int kvx_host_free(void* host_ptr);
+int kvx_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+int kvx_wait_host_word(const volatile int64_t* word, int64_t target, void* stream);
 int kvx_signal_wait(void* stream, const void* d_flag, uint64_t value);
 
 #ifdef __cplusplus

@@ -302,6 +302,34 @@ constexpr int kMaxWarps = 20;  // 20 x 9.7 KB of staging fits the 227 KB opt-in
 constexpr size_t kMinCtaSmem = 120 * 1024;
 constexpr size_t kMaxCtaSmem = 227 * 1024;
 
+// chain_hash with the HIGH words of its four right shifts (x >> 2, >> 30,
+// >> 27, >> 31) computed on the FMA pipe as mul.hi by 2^(32-k) -- one IMAD.HI
+// for each SHF it replaces, so the instruction count is unchanged while the
+// ALU pipe, the step's bound (23 ALU vs 8 FMA-pipe SASS per step), carries
+// four fewer.  The multipliers arrive in registers (a kernel argument) so
+// ptxas cannot fold them back into shifts.  Bit-identical to chain_hash.
+struct HiShift {
+  uint32_t m2, m30, m27, m31;  // 2^30, 2^2, 2^5, 2^1
+};
+__device__ __forceinline__ uint64_t shr64_fma(uint64_t x, int k, uint32_t m) {
+  const uint32_t lo = static_cast<uint32_t>(x), hi = static_cast<uint32_t>(x >> 32);
+  const uint32_t nlo = __funnelshift_r(lo, hi, k);
+  const uint32_t nhi = __umulhi(hi, m);
+  return (static_cast<uint64_t>(nhi) << 32) | nlo;
+}
+template <bool kFma>
+__device__ __forceinline__ int64_t chain_hash_hw(int64_t prev, uint64_t content, const HiShift& k) {
+  if (!kFma) return chain_hash(prev, content);
+  uint64_t x = static_cast<uint64_t>(prev) + 0x9E3779B97F4A7C15ull;
+  x ^= content + 0x9E3779B97F4A7C15ull + (x << 6) + shr64_fma(x, 2, k.m2);
+  x ^= shr64_fma(x, 30, k.m30);
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= shr64_fma(x, 27, k.m27);
+  x *= 0x94D049BB133111EBull;
+  x ^= shr64_fma(x, 31, k.m31);
+  return static_cast<int64_t>(x & 0x7FFFFFFFFFFFFFFFull);
+}
+
 // One 16-step sub-round of one round of one request, written by the
 // prefetching side when it issues the tokens, read by the hashing side.
 struct alignas(16) SubDesc {
@@ -379,8 +407,14 @@ __device__ __forceinline__ void claim(Cursor& c, bool need, int hl, int j, int b
   }
 }
 
+// Token copies carry an L2 evict-first hint: the token stream is read once
+// and must not displace what stays hot in L2 (the instance indices the
+// prefix match probes right after the hash).
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes));
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst),
+               "l"(src), "r"(bytes), "l"(pol));
 }
 
 // Issue the cursor's sub-round into `slot`: lane 0 of the half writes the
@@ -475,11 +509,11 @@ __global__ void __launch_bounds__(1024) order_kernel(const int64_t* __restrict__
 // per step).  V = 1 is the shipped kernel: V = 2 was slower on the Config 4
 // batch at every width, also with a compact (select-only, unroll 4) step loop
 // (profiles/r01/hash_halfwarp.md).
-template <int V>
+template <int V, bool kFma = false>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
     int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
-    const int32_t* __restrict__ order, unsigned long long* ctr, int prio) {
+    const int32_t* __restrict__ order, unsigned long long* ctr, int prio, HiShift hs) {
   extern __shared__ __align__(16) unsigned char hw_smem_raw[];
   WarpSmem<V>& S = reinterpret_cast<WarpSmem<V>*>(hw_smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -592,7 +626,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const uint64_t in = (static_cast<uint64_t>(hi[v][s]) << 32) | lo[v][s];
-          h[v] = chain_hash(h[v], in);
+          h[v] = chain_hash_hw<kFma>(h[v], in, hs);
           if (s == kContentLanes - 1) h14[v] = h[v];
           if (s < kContentLanes && folder && fn[v] > 0) keys[fkb[v] + s] = h[v];
         }
@@ -607,7 +641,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const uint64_t in = (static_cast<uint64_t>(hi[v][s]) << 32) | lo[v][s];
-          const int64_t hn = chain_hash(h[v], in);
+          const int64_t hn = chain_hash_hw<kFma>(h[v], in, hs);
           const bool act = s < lim[v];
           h[v] = act ? hn : h[v];
           if (folder && fn[v] > 0 && act) keys[fkb[v] + s] = h[v];
@@ -776,7 +810,10 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
     }
     if (n_req <= order_max) order = X.order;
     if (!W.hw_attr[dev]) {
-      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1>,
+      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1, false>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(hw::kMaxCtaSmem)));
+      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hw::kMaxCtaSmem)));
       W.hw_attr[dev] = true;
@@ -807,9 +844,16 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
       const char* e = std::getenv("KVX_HASH_PRIO");  // measurement knob: 0 = counter-only claims
       return e ? std::atoi(e) : 1;
     }();
-    KVX_CUDA(cudaLaunchKernelEx(&cfg, hw::halfwarp_hash_kernel<1>, d_tokens, d_tok_off, n_req,
-                                bsi, d_key_off, d_keys, static_cast<const int32_t*>(order), ctr,
-                                order ? prio : 0));
+    static const bool fma_shifts = [] {
+      const char* e = std::getenv("KVX_HASH_FMA");  // measurement knob: high-word shifts on FMA
+      return e && e[0] == '1';
+    }();
+    const hw::HiShift hs{1u << 30, 1u << 2, 1u << 5, 1u << 1};
+    KVX_CUDA(cudaLaunchKernelEx(&cfg,
+                                fma_shifts ? hw::halfwarp_hash_kernel<1, true>
+                                           : hw::halfwarp_hash_kernel<1, false>,
+                                d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
+                                static_cast<const int32_t*>(order), ctr, order ? prio : 0, hs));
     KVX_LAUNCH_CHECK("halfwarp_hash_kernel");
     return KVX_OK;
   }

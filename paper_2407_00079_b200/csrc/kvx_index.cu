@@ -131,6 +131,59 @@ __global__ void __launch_bounds__(256) erase_kernel(int64_t* __restrict__ tkeys,
     atomicAdd(&ctr->live, static_cast<unsigned long long>(-static_cast<long long>(removed)));
 }
 
+// Erase keys [0, ne) and insert keys [ne, ne + ni) in ONE launch (the drop-in
+// block manager's put: evicted ids out, new ids in).  Safe to run together:
+// inserts claim only EMPTY slots (never tombstones) and stop at their own key,
+// an erase only turns its own key into a tombstone, and the two sets are
+// disjoint (a block being admitted is never its own victim).
+__global__ void __launch_bounds__(256) update_kernel(int64_t* __restrict__ tkeys,
+                                                     int64_t* __restrict__ tvals, uint64_t mask,
+                                                     const int64_t* __restrict__ erase, int64_t ne,
+                                                     const int64_t* __restrict__ ins,
+                                                     const int64_t* __restrict__ vals, int64_t ni,
+                                                     Counters* __restrict__ ctr) {
+  unsigned long long added = 0, removed = 0, rejected = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < ne + ni;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i < ne) {
+      const int64_t key = erase[i];
+      if (is_reserved(key)) continue;
+      uint64_t s = mix64(static_cast<uint64_t>(key)) & mask;
+      while (true) {
+        const int64_t cur = tkeys[s];
+        if (cur == kKeyEmpty) break;
+        if (cur == key) {
+          const int64_t prev = static_cast<int64_t>(
+              atomicCAS(reinterpret_cast<unsigned long long*>(tkeys + s),
+                        static_cast<unsigned long long>(key),
+                        static_cast<unsigned long long>(kKeyTomb)));
+          if (prev == key) ++removed;
+          break;
+        }
+        s = (s + 1) & mask;
+      }
+    } else {
+      const int64_t j = i - ne;
+      const int64_t key = ins[j];
+      if (is_reserved(key)) {
+        ++rejected;
+        continue;
+      }
+      insert_one(tkeys, tvals, mask, key, vals ? vals[j] : j, added);
+    }
+  }
+  added = warp_sum(added);
+  removed = warp_sum(removed);
+  rejected = warp_sum(rejected);
+  if ((threadIdx.x & 31) == 0) {
+    if (added != removed)
+      atomicAdd(&ctr->live, static_cast<unsigned long long>(static_cast<long long>(added) -
+                                                            static_cast<long long>(removed)));
+    if (added) atomicAdd(&ctr->used, added);
+    if (rejected) atomicAdd(&ctr->rejected, rejected);
+  }
+}
+
 __device__ __forceinline__ int64_t find_slot(const int64_t* __restrict__ tkeys, uint64_t mask,
                                              int64_t key) {
   if (is_reserved(key)) return -1;
@@ -237,6 +290,26 @@ __device__ __forceinline__ unsigned long long pack_best(int64_t len, int32_t id)
   return (static_cast<unsigned long long>(len) << 32) | static_cast<unsigned long long>(~ordered);
 }
 
+// The per-task epilogue shared by both match kernels (lane 0 of the warp /
+// thread 0 of the CTA that owns the task).
+__device__ __forceinline__ void match_result(const MatchParams& p, int64_t t, int64_t r, int i,
+                                             int64_t len, int64_t* __restrict__ len_out,
+                                             int64_t* __restrict__ best_len,
+                                             int32_t* __restrict__ best_id) {
+  if (len_out) len_out[t] = len;
+  if (p.n_dests > 0) {
+    const unsigned long long v = pack_best(len, p.ids[i]);
+    for (int j = 0; j < p.n_dests; ++j) atomicMax(p.dests[j] + r, v);
+  } else if (best_len) {
+    if (p.n_inst == 1 && !p.packed_only) {
+      best_len[r] = len;
+      best_id[r] = p.ids[0];
+    } else {
+      atomicMax(reinterpret_cast<unsigned long long*>(best_len + r), pack_best(len, p.ids[i]));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ MatchParams p,
                                                     const int64_t* __restrict__ keys,
                                                     const int64_t* __restrict__ key_off,
@@ -281,20 +354,69 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
       }
       if (stop) break;
     }
-    if (lane == 0) {
-      if (len_out) len_out[t] = len;
-      if (p.n_dests > 0) {
-        const unsigned long long v = pack_best(len, p.ids[i]);
-        for (int j = 0; j < p.n_dests; ++j) atomicMax(p.dests[j] + r, v);
-      } else if (best_len) {
-        if (p.n_inst == 1 && !p.packed_only) {
-          best_len[r] = len;
-          best_id[r] = p.ids[0];
-        } else {
-          atomicMax(reinterpret_cast<unsigned long long*>(best_len + r), pack_best(len, p.ids[i]));
+    if (lane == 0) match_result(p, t, r, i, len, len_out, best_len, best_id);
+  }
+}
+
+// K2 with G warps per (request, instance) task: the request's 128-key
+// windows go to the warps in waves (window = wave * G + warp), so a long
+// matched prefix costs ceil(windows / G) dependent probe rounds instead of
+// one per window; each warp's first miss is folded into a shared atomicMin,
+// and the task ends after the first wave whose windows all lie past it (all
+// windows before the minimum were fully probed: it IS the first miss).  The
+// extra probes are the speculative windows of the wave that holds the miss.
+template <int G>
+__global__ void __launch_bounds__(G * 32) match_group_kernel(
+    const __grid_constant__ MatchParams p, const int64_t* __restrict__ keys,
+    const int64_t* __restrict__ key_off, int64_t n_req, int64_t* __restrict__ len_out,
+    int64_t* __restrict__ best_len, int32_t* __restrict__ best_id) {
+  __shared__ long long first_miss;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int64_t kWin = 32 * kProbeChains;
+  const int64_t tasks = n_req * p.n_inst;
+  for (int64_t t = blockIdx.x; t < tasks; t += gridDim.x) {
+    const int64_t r = tasks <= 0xFFFFFFFFll
+                          ? static_cast<int64_t>(static_cast<uint32_t>(t) / static_cast<uint32_t>(p.n_inst))
+                          : t / p.n_inst;
+    const int i = static_cast<int>(t - r * p.n_inst);
+    const int64_t* __restrict__ tk = p.keys[i];
+    const uint64_t mask = p.mask[i];
+    const int64_t base = key_off[r];
+    const int64_t n = key_off[r + 1] - base;
+    const int64_t* __restrict__ q = keys + base;
+    if (threadIdx.x == 0) first_miss = n;  // no miss: the whole chain matches
+    __syncthreads();
+    for (int64_t wave = 0;; ++wave) {
+      const int64_t k0 = (wave * G + warp) * kWin;
+      if (k0 < n && k0 < static_cast<int64_t>(*reinterpret_cast<volatile long long*>(&first_miss))) {
+        int64_t qk[kProbeChains];
+        bool qv[kProbeChains], hit[kProbeChains];
+#pragma unroll
+        for (int j = 0; j < kProbeChains; ++j) {
+          const int64_t idx = k0 + 32 * j + lane;
+          qv[j] = idx < n;
+          qk[j] = qv[j] ? __ldg(q + idx) : 0;
+        }
+        probe_multi<kProbeChains>(tk, mask, qk, qv, hit);
+#pragma unroll
+        for (int j = 0; j < kProbeChains; ++j) {
+          const unsigned miss = __ballot_sync(0xffffffffu, !hit[j] && qv[j]);
+          if (miss) {  // the window's first miss (out-of-range lanes are not misses here)
+            if (lane == 0) atomicMin(&first_miss, static_cast<long long>(k0 + 32 * j + __ffs(miss) - 1));
+            break;
+          }
         }
       }
+      __syncthreads();
+      const int64_t fm = static_cast<int64_t>(first_miss);
+      const int64_t covered = (wave + 1) * G * kWin;
+      if (fm < covered || covered >= n) break;  // uniform over the CTA
     }
+    if (threadIdx.x == 0) {
+      const int64_t len = static_cast<int64_t>(first_miss);
+      match_result(p, t, r, i, len, len_out, best_len, best_id);
+    }
+    __syncthreads();  // first_miss is re-initialised for the next task
   }
 }
 
@@ -477,6 +599,51 @@ int kvx_index_erase(kvx_index* x, const int64_t* d_keys, int64_t n, void* stream
   return KVX_OK;
 }
 
+int kvx_index_update(kvx_index* x, const int64_t* d_erase, int64_t ne, const int64_t* d_insert,
+                     const int64_t* d_values, int64_t ni, void* stream) {
+  KVX_REQUIRE(x != nullptr, "kvx_index_update: NULL index");
+  KVX_REQUIRE(ne >= 0 && ni >= 0, "kvx_index_update: counts must be >= 0");
+  if (ne + ni == 0) return KVX_OK;
+  KVX_REQUIRE((ne == 0 || d_erase) && (ni == 0 || d_insert), "kvx_index_update: NULL keys");
+  DeviceGuard g(x->device);
+  cudaStream_t s = as_stream(stream);
+  if (ni) {
+    int st = ensure_room(x, ni, s);
+    if (st) return st;
+  }
+  update_kernel<<<grid_for(ne + ni, 256, x->device), 256, 0, s>>>(
+      x->keys, x->vals, static_cast<uint64_t>(x->slots - 1), d_erase, ne, d_insert, d_values, ni,
+      x->ctr);
+  KVX_LAUNCH_CHECK("update_kernel");
+  x->used_ub += ni;
+  return KVX_OK;
+}
+
+int kvx_index_l2_pin(const kvx_index* x, void* stream, int on) {
+  KVX_REQUIRE(x != nullptr && stream != nullptr, "kvx_index_l2_pin: NULL index or stream");
+  DeviceGuard g(x->device);
+  cudaStreamAttrValue attr = {};
+  if (on) {
+    int max_persist = 0, max_window = 0;
+    KVX_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, x->device));
+    KVX_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, x->device));
+    KVX_REQUIRE(max_persist > 0 && max_window > 0, "kvx_index_l2_pin: no persisting L2 on this device");
+    const size_t bytes = static_cast<size_t>(x->slots) * sizeof(int64_t);
+    const size_t window = std::min(bytes, static_cast<size_t>(max_window));
+    const size_t carve = std::min(window, static_cast<size_t>(max_persist));
+    size_t cur = 0;
+    KVX_CUDA(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+    if (cur < carve) KVX_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+    attr.accessPolicyWindow.base_ptr = x->keys;
+    attr.accessPolicyWindow.num_bytes = window;
+    attr.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, double(carve) / double(window)));
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  }
+  KVX_CUDA(cudaStreamSetAttribute(as_stream(stream), cudaStreamAttributeAccessPolicyWindow, &attr));
+  return KVX_OK;
+}
+
 int kvx_index_lookup(const kvx_index* x, const int64_t* d_keys, int64_t n, int64_t* d_out,
                      void* stream) {
   KVX_REQUIRE(x != nullptr, "kvx_index_lookup: NULL index");
@@ -600,14 +767,38 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
   cudaStream_t s = as_stream(stream);
   if (d_best_len && (n_inst > 1 || packed_only) && n_dests == 0)
     KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
-  const int threads = 256;
   const int64_t tasks = n_req * n_inst;
+  static const int group = [] {
+    const char* e = std::getenv("KVX_MATCH_GROUP");  // warps per task (1 = warp-per-task kernel)
+    const int v = e ? std::atoi(e) : 4;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 4;
+  }();
+  if (group > 1) {
+    const int64_t cap = static_cast<int64_t>(sm_count(dev)) * (64 / group);  // 2048 threads / SM
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(tasks, cap)));
+    switch (group) {
+      case 2:
+        match_group_kernel<2><<<blocks, 64, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out,
+                                                    d_best_len, d_best_id);
+        break;
+      case 8:
+        match_group_kernel<8><<<blocks, 256, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out,
+                                                     d_best_len, d_best_id);
+        break;
+      default:
+        match_group_kernel<4><<<blocks, 128, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out,
+                                                     d_best_len, d_best_id);
+    }
+    KVX_LAUNCH_CHECK("match_group_kernel");
+  } else {
+  const int threads = 256;
   const int64_t want = (tasks + (threads / 32) - 1) / (threads / 32);
   const int64_t cap = static_cast<int64_t>(sm_count(dev)) * 16;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(want, cap)));
   match_kernel<<<blocks, threads, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out, d_best_len,
                                           d_best_id);
   KVX_LAUNCH_CHECK("match_kernel");
+  }
   if (d_best_len && n_inst > 1 && !packed_only) {
     unpack_best_kernel<<<grid_for(n_req, 256, dev), 256, 0, s>>>(
         reinterpret_cast<const unsigned long long*>(d_best_len), d_best_len, d_best_id, n_req);

@@ -262,6 +262,62 @@ int kvx_enable_peer(int device, int peer_device) {
   return KVX_OK;
 }
 
+// ---- small host-side plumbing for C / C++ hosts (no CUDA runtime of their own) --
+
+int kvx_stream_create(int device, void** out) {
+  KVX_REQUIRE(out != nullptr, "kvx_stream_create: NULL out");
+  DeviceGuard g(device);
+  cudaStream_t s = nullptr;
+  KVX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = s;
+  return KVX_OK;
+}
+
+int kvx_stream_destroy(void* stream) {
+  if (!stream) return KVX_OK;
+  KVX_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  KVX_CUDA(cudaStreamDestroy(as_stream(stream)));
+  return KVX_OK;
+}
+
+int kvx_host_alloc(int64_t bytes, void** out) {
+  KVX_REQUIRE(out && bytes > 0, "kvx_host_alloc: bad arguments");
+  KVX_CUDA(cudaHostAlloc(out, static_cast<size_t>(bytes),
+                         cudaHostAllocPortable | cudaHostAllocMapped));
+  return KVX_OK;
+}
+
+int kvx_host_free(void* p) {
+  if (p) KVX_CUDA(cudaFreeHost(p));
+  return KVX_OK;
+}
+
+int kvx_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  KVX_REQUIRE(bytes >= 0 && (bytes == 0 || (dst && src)), "kvx_memcpy_async: bad arguments");
+  if (bytes) KVX_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault,
+                                      as_stream(stream)));
+  return KVX_OK;
+}
+
+int kvx_wait_host_word(const volatile int64_t* word, int64_t target, void* stream) {
+  KVX_REQUIRE(word != nullptr, "kvx_wait_host_word: NULL word");
+  // Spin on the pinned word the GPU writes (a kernel result or a stream-
+  // ordered flag) until it reaches `target`: no synchronise call on the fast
+  // path.  Every 4096 polls the stream is asked whether it failed, or went
+  // idle without writing.
+  for (uint64_t i = 1;; ++i) {
+    if (*word >= target) return KVX_OK;
+    if ((i & 4095) == 0) {
+      cudaError_t e = cudaStreamQuery(as_stream(stream));
+      if (e == cudaSuccess) {
+        if (*word >= target) return KVX_OK;
+        return set_error(KVX_ECUDA, "kvx_wait_host_word: stream idle, word never written");
+      }
+      if (e != cudaErrorNotReady) return cuda_error(e, "kvx_wait_host_word");
+    }
+  }
+}
+
 int kvx_signal_write(void* stream, void* d_flag, uint64_t value) {
   KVX_REQUIRE(d_flag != nullptr, "kvx_signal_write: NULL flag");
   int st = memops_ready();

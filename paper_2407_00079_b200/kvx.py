@@ -99,6 +99,7 @@ _sig("kvx_index_insert", C.c_int, _vp, _vp, _vp, _i64, _vp)
 _sig("kvx_index_erase", C.c_int, _vp, _vp, _i64, _vp)
 _sig("kvx_index_lookup", C.c_int, _vp, _vp, _i64, _vp, _vp)
 _sig("kvx_index_clear", C.c_int, _vp, _vp)
+_sig("kvx_index_l2_pin", C.c_int, _vp, _vp, C.c_int)
 _sig("kvx_index_reserve", C.c_int, _vp, _i64, _vp)
 _sig("kvx_index_stats", C.c_int, _vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
      C.POINTER(_i64), _vp)
@@ -306,6 +307,11 @@ class BlockIndex:
 
     def reserve(self, min_keys: int, stream=None):
         check(_L.kvx_index_reserve(self.h, min_keys, _stream(stream)))
+
+    def l2_pin(self, stream, on: bool = True):
+        """Keep the key table L2-resident for kernels on `stream` (persisting
+        access-policy window)."""
+        check(_L.kvx_index_l2_pin(self.h, _stream(stream), int(on)))
 
     def stats(self, stream=None):
         live, tomb, slots, rej = _i64(), _i64(), _i64(), _i64()
