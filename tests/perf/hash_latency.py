@@ -17,7 +17,8 @@ from oracle import Oracle  # noqa: E402
 T = int(os.environ.get("HL_TOKENS", "24576"))
 o = Oracle()
 rng = np.random.default_rng(0)
-for n in [1, 2, 32, 148, 296, 592, 1184, 1776, 2368, 3552, 4096]:
+NS = [int(x) for x in os.environ.get("HL_NS", "1,2,32,148,296,592,1184,1776,2368,3552,4096").split(",")]
+for n in NS:
     lens = np.full(n, T, dtype=np.int64)
     tok_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
     tokens = rng.integers(0, 32000, size=int(tok_off[-1])).astype(np.int32)
