@@ -660,8 +660,45 @@ def run_kvx(args):
 
     peaks = measured_peaks()
     roof = None
-    if klaunches:
-        kname = "copy_tma_kernel" if args.copy_impl == "tma" else "copy_lsu_kernel"
+    kname = "copy_tma_kernel" if args.copy_impl == "tma" else "copy_lsu_kernel"
+    traffic = ncu_traffic(kname)
+    ms_step = ms_total / args.steps
+    if mode in ("local_fused", "local_staged"):
+        # In-step roofline (primary): on one GPU the step is nothing but the
+        # copy launches (local_fused: one per unit; staged: gather + scatter),
+        # overlapped by programmatic dependent launch, so algorithmic bytes
+        # per step / step time IS the copy kernel's in-step throughput; the
+        # per-launch figures below divide it back out.
+        per_step = units_per_step * (1 if mode == "local_fused" else 2)
+        alg_step = 2.0 * plan["payload_total"] * (1 if mode == "local_fused" else 2)
+        achieved = alg_step / (ms_step / 1e3) / GB
+        peak = peaks["hbm_gbs"]
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": kname,
+                "how": "in-step: algorithmic bytes of every copy launch of the timed steps "
+                       "(2 x payload: read + write) / the steps' CUDA-event time",
+                "launches_per_step": per_step,
+                "algorithmic_bytes_per_launch": alg_step / per_step,
+                "avg_launch_ms_in_step": ms_step / per_step,
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"}
+        if (traffic and mode == "local_fused" and args.config == 2 and args.block_size == 16
+                and args.dtype_bytes == 2):
+            # ncu DRAM bytes of this launch shape (one wave, one layer: 1 GiB
+            # algorithmic); the 16 requests of a wave re-read their shared 256-
+            # block prefix inside one launch, so ~40% of the reads hit L2
+            dram = traffic * per_step / (ms_step / 1e3) / GB
+            roof.update({"dram_achieved": dram, "dram_frac": dram / peak,
+                         "dram_note": "ncu dram__bytes_read+write per launch "
+                                      "(profiles/ncu_traffic.json) x launches per step / step "
+                                      "time: below the algorithmic bytes because shared-prefix "
+                                      "reads hit L2"})
+        if klaunches:
+            roof["isolated_launch"] = {
+                "avg_ms": kavg, "achieved": kbytes / (kavg / 1e3) / GB,
+                "frac": kbytes / (kavg / 1e3) / GB / peak, "launches_timed": klaunches,
+                "note": "every 20th launch bracketed by CUDA events, which serialises it "
+                        "(no overlap with its neighbours)"}
+    elif klaunches:
         achieved = kbytes / (kavg / 1e3) / GB
         if mode in ("peer_fused", "peer_pull"):
             bound, peak, pk_src = "nvlink", link_gbs, ("measured in this run: 1 GiB copy-engine "
@@ -669,26 +706,16 @@ def run_kvx(args):
         else:
             bound, peak = "hbm", peaks["hbm_gbs"]
             pk_src = f"MEASURED_PEAKS.json hbm_gbs ({peaks['src']})"
-        role_kernel = {"local_fused": "fused paged copy", "local_staged": "gather",
-                       "peer_ce": "gather (prefill GPU)", "peer_fused": "peer paged copy",
+        role_kernel = {"peer_ce": "gather (prefill GPU)", "peer_fused": "peer paged copy",
                        "peer_pull": "paged copy pulling from the prefill GPU"}
-        traffic = ncu_traffic(kname)
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "kernel": kname,
                 "launch_role": role_kernel.get(mode), "avg_launch_ms": kavg,
                 "launches_timed": klaunches,
                 "algorithmic_bytes_per_launch": kbytes,
+                "how": "sampled launches bracketed by CUDA events (the step itself is "
+                       "link-bound: see `link`)",
                 "peak_source": pk_src}
-        if (traffic and mode == "local_fused" and args.config == 2 and args.block_size == 16
-                and args.dtype_bytes == 2):
-            # the ncu capture is of this launch shape (one wave = 512 MiB of payload):
-            # half of every request is the shared hot prefix, which 16 requests of a
-            # wave re-read inside one launch, so ~40% of the algorithmic reads hit L2
-            dram = traffic / (kavg / 1e3) / GB
-            roof.update({"dram_achieved": dram, "dram_frac": dram / peak,
-                         "dram_note": "ncu dram__bytes per launch (profiles/ncu_traffic.json) / "
-                                      "the same launch time; below the algorithmic bytes because "
-                                      "the shared-prefix reads hit L2"})
 
     if rank == 0:
         line = {

@@ -19,6 +19,7 @@
 // the B200 block index (libkvx: kvx_match_prefix_batch / kvx_index_lookup);
 // every put mirrors its inserted and evicted ids into that index.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -113,14 +114,17 @@ void* shared_stream() {
 
 // Per-process call statistics (KVCSIM_GPU_STATS=1 prints them at exit).
 struct Stats {
-  uint64_t queries = 0, cached = 0, updates = 0;
+  uint64_t queries = 0, cached = 0, updates = 0, pools = 0, recycled = 0;
+  double query_s = 0, update_s = 0, pool_s = 0;
   ~Stats() {
     if (std::getenv("KVCSIM_GPU_STATS"))
-      std::fprintf(stderr, "kvcsim gpu: %llu queries (%llu answered from the per-version cache), "
-                           "%llu index updates\n",
-                   static_cast<unsigned long long>(queries),
-                   static_cast<unsigned long long>(cached),
-                   static_cast<unsigned long long>(updates));
+      std::fprintf(stderr,
+                   "kvcsim gpu: %llu queries (%llu from the per-version cache) %.1f us avg, "
+                   "%llu index updates %.1f us avg, %llu pools (%llu recycled) %.1f us avg\n",
+                   static_cast<unsigned long long>(queries), static_cast<unsigned long long>(cached),
+                   queries ? 1e6 * query_s / queries : 0.0, static_cast<unsigned long long>(updates),
+                   updates ? 1e6 * update_s / updates : 0.0, static_cast<unsigned long long>(pools),
+                   static_cast<unsigned long long>(recycled), pools ? 1e6 * pool_s / pools : 0.0);
   }
 };
 Stats& stats() {
@@ -128,15 +132,59 @@ Stats& stats() {
   return st;
 }
 
+struct Timer {
+  double& acc;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit Timer(double& a) : acc(a) {}
+  ~Timer() {
+    acc += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+};
+
+// Device resources of destroyed pools, reused by new ones: creating a GPU
+// index and a pinned arena costs allocations and a device synchronise, and
+// engines (and the reference's tests) create many short-lived pools.  Never
+// freed at exit (process teardown releases them).
+struct Recycled {
+  kvx_index* idx;
+  int64_t* arena;
+  std::size_t half;
+  uint64_t next_op;
+};
+std::vector<Recycled>& recycle_bin() {
+  static auto* bin = new std::vector<Recycled>();
+  return *bin;
+}
+
 class DeviceIndex {
  public:
   DeviceIndex() : dev_(selected_device()), stream_(shared_stream()) {
+    Timer t(stats().pool_s);
+    ++stats().pools;
+    auto& bin = recycle_bin();
+    if (!bin.empty()) {  // an emptied index and its arena from a destroyed pool
+      const Recycled r = bin.back();
+      bin.pop_back();
+      idx_ = r.idx;
+      arena_ = r.arena;
+      half_ = r.half;
+      next_op_ = r.next_op;
+      ++stats().recycled;
+      return;
+    }
     ok(kvx_index_create(dev_, 0, &idx_), "kvx_index_create");
     grow(256);
   }
   ~DeviceIndex() {
-    if (stream_) kvx_sync(stream_);  // nothing in flight reads the arena any more
-    if (idx_) kvx_index_destroy(idx_);
+    if (!idx_) return;
+    // emptied on the shared stream (ordered before any later use of it);
+    // the arena's ops counter travels with it
+    if (kvx_index_clear(idx_, stream_) == KVX_OK) {
+      recycle_bin().push_back({idx_, arena_, half_, next_op_});
+      return;
+    }
+    kvx_sync(stream_);
+    kvx_index_destroy(idx_);
     if (arena_) kvx_host_free(arena_);
   }
   DeviceIndex(const DeviceIndex&) = delete;
@@ -146,6 +194,7 @@ class DeviceIndex {
 
   void apply(const std::vector<BlockId>& erase, const std::vector<BlockId>& insert) {
     if (erase.empty() && insert.empty()) return;
+    Timer t(stats().update_s);
     const std::size_t ne = erase.size(), ni = insert.size();
     int64_t* buf = stage(ne + ni);
     std::memcpy(buf, erase.data(), ne * sizeof(int64_t));
@@ -159,6 +208,7 @@ class DeviceIndex {
 
   std::size_t match(std::span<const BlockId> blocks) const {
     if (blocks.empty()) return 0;
+    Timer t(stats().query_s);
     const std::size_t n = blocks.size();
     ++stats().queries;
     // the reference's conductor asks each pool the same chain twice per
@@ -188,6 +238,7 @@ class DeviceIndex {
   }
 
   bool contains(BlockId id) const {
+    Timer t(stats().query_s);
     ++stats().queries;
     int64_t* buf = stage(1);
     buf[0] = id;

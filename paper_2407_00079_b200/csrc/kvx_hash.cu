@@ -663,6 +663,201 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel(
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
+// ---- K1b, software-pipelined control ---------------------------------------
+// The same half-warp algorithm with the per-sub-round bookkeeping taken off
+// the key chain's critical path.  In halfwarp_hash_kernel a lone warp runs a
+// 1,536-block request at ~156 cycles per step against ~107 for the bare
+// chain_hash chain: each 16-step sub-round first issues the next prefetch,
+// waits, reads its descriptor, votes, branches -- in program order, before
+// the first chain step.  Here iteration `it` runs the 16 chain steps of
+// sub-round it with everything sub-round it+1 needs computed in the SAME
+// branch-free basic block (predicated cp.async and descriptor stores,
+// cursor advance by selects, the it+1 descriptor read and its two votes), so
+// the instruction scheduler hides that work in the chain's idle issue slots;
+// only the rare claim of a new request stays behind a branch.
+__device__ __forceinline__ void cp_async16_pred(uint32_t dst, const void* src, int bytes, bool on) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " @p cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n}\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "l"(pol), "r"(static_cast<int>(on)));
+}
+
+// Branch-free issue of the cursor's sub-round into `slot` (see issue()).
+__device__ __forceinline__ void issue_p(const Cursor& c, HalfSmem& H, int slot, int hl, int j,
+                                        int bs, int nsub, const int32_t* tokens) {
+  const int nb = c.live ? min(kContentLanes, c.nblk - kContentLanes * c.k) : 0;
+  SubDesc d;
+  d.rem0 = c.ntok - kContentLanes * c.k * bs - 16 * c.u;
+  d.nb = nb;
+  d.flags = (c.u == 0 ? 1 : 0) | (c.u == nsub - 1 ? 2 : 0) | (c.k == 0 ? 4 : 0);
+  d.m = c.m;
+  d.kb = c.kb0 + static_cast<int64_t>(kContentLanes) * c.k;
+  d.pad = 0;
+  if (hl == 0) H.desc[slot] = d;  // predicated stores
+  const bool copy = j >= 0 && j < nb;
+  const int row = copy ? j : 0;
+  const uint32_t dst =
+      static_cast<uint32_t>(__cvta_generic_to_shared(&H.tok[slot][row * kRowWords]));
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int bytes = max(0, min(4, c.prem - 4 * q)) * 4;
+    cp_async16_pred(dst + 16 * q, bytes ? static_cast<const void*>(c.a + 4 * q)
+                                        : static_cast<const void*>(tokens),
+                    bytes, copy);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Branch-free cursor advance (see step_cursor); true when the request's
+// last round was issued (a new request must be claimed).
+__device__ __forceinline__ bool step_cursor_p(Cursor& c, int bs, int nsub) {
+  const bool live = c.live;
+  const int u1 = c.u + 1;
+  const bool wrap = u1 >= nsub;
+  const int adv = live ? (wrap ? 14 * bs + 16 : 16) : 0;
+  c.u = live ? (wrap ? 0 : u1) : c.u;
+  c.k += (live && wrap) ? 1 : 0;
+  c.a += adv;
+  c.prem -= adv;
+  return live && wrap && kContentLanes * c.k >= c.nblk;
+}
+
+// What the lanes of a half need to run one sub-round.
+struct Ctl {
+  const uint32_t* lo;
+  const uint32_t* hi;
+  int lim;        // steps that count for this lane (16 on the fast path)
+  int nb, flags;  // of the sub-round's descriptor
+  int64_t kb;
+  bool fast, idle;
+};
+
+__device__ __forceinline__ Ctl make_ctl(HalfSmem& H, const uint32_t* zero, int slot, bool folder,
+                                        int j, int bs, int fn_next) {
+  const SubDesc d = H.desc[slot];
+  Ctl c;
+  c.nb = d.nb;
+  c.flags = d.flags;
+  c.kb = d.kb;
+  if (folder) {
+    c.lo = H.clo;
+    c.hi = H.chi;
+    c.lim = fn_next;
+  } else {
+    c.lo = &H.tok[slot][j * kRowWords + d.m];
+    c.hi = zero;
+    c.lim = j < d.nb ? max(0, min(16, d.rem0 - j * bs)) : 16;
+  }
+  const bool fast = folder ? (fn_next == 0 || fn_next == kContentLanes) : c.lim == 16;
+  c.fast = __all_sync(0xffffffffu, fast);
+  c.idle = __all_sync(0xffffffffu, d.nb == 0 && fn_next == 0);
+  return c;
+}
+
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
+    const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
+    int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
+    const int32_t* __restrict__ order, unsigned long long* ctr, int prio) {
+  extern __shared__ __align__(16) unsigned char hw_smem_raw[];
+  WarpSmem<1>& S = reinterpret_cast<WarpSmem<1>*>(hw_smem_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int half = lane >> 4;
+  const int hl = lane & 15;
+  const int j = hl - 1;
+  const bool folder = hl == 0;
+  const int nsub = bs >> 4;
+  HalfSmem& H = S.h[0][half];
+  if (lane < 16) S.zero[lane] = 0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  const int nwarps = static_cast<int>(blockDim.x >> 5), warp = static_cast<int>(threadIdx.x >> 5);
+  const unsigned long long halves = 2ull * nwarps * gridDim.x;
+  unsigned long long first =
+      prio ? (static_cast<unsigned long long>(nwarps - 1 - warp) * gridDim.x + blockIdx.x) * 2 + half
+           : ~0ull;
+  const unsigned long long base = prio ? halves : 0ull;
+
+  Cursor P;
+  P.live = false;
+  P.a = tokens;
+  P.prem = P.ntok = P.nblk = P.k = P.u = P.m = 0;
+  P.kb0 = 0;
+  claim(P, true, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
+#pragma unroll 1
+  for (int i = 0; i < kPrefetch; ++i) {
+    issue_p(P, H, i, hl, j, bs, nsub, tokens);
+    const bool need = step_cursor_p(P, bs, nsub);
+    if (__any_sync(0xffffffffu, need))
+      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
+  }
+  // sub-round 0's tokens and control
+  asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
+  __syncwarp();
+  int fn = 0, freset = 0;  // folds of the current sub-round (the previous round's blocks)
+  int64_t fkb = 0;
+  Ctl c = make_ctl(H, S.zero, 0, folder, j, bs, 0);
+  int64_t h = 0;
+#pragma unroll 1
+  for (uint32_t it = 0;; ++it) {
+    if (c.idle) break;
+    if (folder) {
+      if (freset && fn > 0) h = 0;
+    } else if (c.flags & 1) {
+      h = 0;
+    }
+    // the folder's work in sub-round it+1: the blocks of the round finishing now
+    const bool round_done = c.nb > 0 && (c.flags & 2);
+    const int fn_next = round_done ? c.nb : 0;
+    const int nslot = static_cast<int>((it + 1) % kSlots);
+    Ctl cn;
+    bool need;
+    if (c.fast) {
+      int64_t h0 = h, h14 = h;
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const uint64_t in = (static_cast<uint64_t>(c.hi[s]) << 32) | c.lo[s];
+        h = chain_hash(h, in);
+        if (s == kContentLanes - 1) h14 = h;
+        if (s < kContentLanes && folder && fn > 0) keys[fkb + s] = h;
+      }
+      if (folder) h = fn > 0 ? h14 : h0;
+      // next sub-round's work, scheduled into the chain's idle issue slots
+      issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
+      need = step_cursor_p(P, bs, nsub);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
+      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
+    } else {
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const uint64_t in = (static_cast<uint64_t>(c.hi[s]) << 32) | c.lo[s];
+        const int64_t hn = chain_hash(h, in);
+        const bool act = s < c.lim;
+        h = act ? hn : h;
+        if (folder && fn > 0 && act) keys[fkb + s] = h;
+      }
+      issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
+      need = step_cursor_p(P, bs, nsub);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
+      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
+    }
+    // hand the finished round's contents to the folder (read next sub-round)
+    if (round_done && !folder) {
+      H.clo[j] = static_cast<uint32_t>(h);
+      H.chi[j] = static_cast<uint32_t>(static_cast<uint64_t>(h) >> 32);
+    }
+    fn = fn_next;
+    fkb = c.kb;
+    freset = c.flags & 4;
+    __syncwarp();
+    if (__any_sync(0xffffffffu, need))
+      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
+    c = cn;
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 }  // namespace hw
 
 // Claim counters and the longest-first order are per (device, stream):
@@ -816,6 +1011,9 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
       KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hw::kMaxCtaSmem)));
+      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(hw::kMaxCtaSmem)));
       W.hw_attr[dev] = true;
     }
     if (order) {
@@ -849,11 +1047,21 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
       return e && e[0] == '1';
     }();
     const hw::HiShift hs{1u << 30, 1u << 2, 1u << 5, 1u << 1};
-    KVX_CUDA(cudaLaunchKernelEx(&cfg,
-                                fma_shifts ? hw::halfwarp_hash_kernel<1, true>
-                                           : hw::halfwarp_hash_kernel<1, false>,
-                                d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
-                                static_cast<const int32_t*>(order), ctr, order ? prio : 0, hs));
+    static const int pipelined = [] {
+      const char* e = std::getenv("KVX_HASH_PIPE");  // 0: the r01 loop (measurement knob)
+      return e ? std::atoi(e) : 1;
+    }();
+    if (pipelined) {
+      KVX_CUDA(cudaLaunchKernelEx(&cfg, hw::halfwarp_hash_kernel_p, d_tokens, d_tok_off, n_req,
+                                  bsi, d_key_off, d_keys, static_cast<const int32_t*>(order), ctr,
+                                  order ? prio : 0));
+    } else {
+      KVX_CUDA(cudaLaunchKernelEx(&cfg,
+                                  fma_shifts ? hw::halfwarp_hash_kernel<1, true>
+                                             : hw::halfwarp_hash_kernel<1, false>,
+                                  d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
+                                  static_cast<const int32_t*>(order), ctr, order ? prio : 0, hs));
+    }
     KVX_LAUNCH_CHECK("halfwarp_hash_kernel");
     return KVX_OK;
   }

@@ -365,14 +365,14 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
 // and the task ends after the first wave whose windows all lie past it (all
 // windows before the minimum were fully probed: it IS the first miss).  The
 // extra probes are the speculative windows of the wave that holds the miss.
-template <int G>
+template <int G, int C>
 __global__ void __launch_bounds__(G * 32) match_group_kernel(
     const __grid_constant__ MatchParams p, const int64_t* __restrict__ keys,
     const int64_t* __restrict__ key_off, int64_t n_req, int64_t* __restrict__ len_out,
     int64_t* __restrict__ best_len, int32_t* __restrict__ best_id) {
   __shared__ long long first_miss;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int64_t kWin = 32 * kProbeChains;
+  constexpr int64_t kWin = 32 * C;
   const int64_t tasks = n_req * p.n_inst;
   for (int64_t t = blockIdx.x; t < tasks; t += gridDim.x) {
     const int64_t r = tasks <= 0xFFFFFFFFll
@@ -389,17 +389,17 @@ __global__ void __launch_bounds__(G * 32) match_group_kernel(
     for (int64_t wave = 0;; ++wave) {
       const int64_t k0 = (wave * G + warp) * kWin;
       if (k0 < n && k0 < static_cast<int64_t>(*reinterpret_cast<volatile long long*>(&first_miss))) {
-        int64_t qk[kProbeChains];
-        bool qv[kProbeChains], hit[kProbeChains];
+        int64_t qk[C];
+        bool qv[C], hit[C];
 #pragma unroll
-        for (int j = 0; j < kProbeChains; ++j) {
+        for (int j = 0; j < C; ++j) {
           const int64_t idx = k0 + 32 * j + lane;
           qv[j] = idx < n;
           qk[j] = qv[j] ? __ldg(q + idx) : 0;
         }
-        probe_multi<kProbeChains>(tk, mask, qk, qv, hit);
+        probe_multi<C>(tk, mask, qk, qv, hit);
 #pragma unroll
-        for (int j = 0; j < kProbeChains; ++j) {
+        for (int j = 0; j < C; ++j) {
           const unsigned miss = __ballot_sync(0xffffffffu, !hit[j] && qv[j]);
           if (miss) {  // the window's first miss (out-of-range lanes are not misses here)
             if (lane == 0) atomicMin(&first_miss, static_cast<long long>(k0 + 32 * j + __ffs(miss) - 1));
@@ -768,27 +768,36 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
   if (d_best_len && (n_inst > 1 || packed_only) && n_dests == 0)
     KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
   const int64_t tasks = n_req * n_inst;
+  // warps per task x probe chains per lane (measured, profiles/r02/match.md)
   static const int group = [] {
-    const char* e = std::getenv("KVX_MATCH_GROUP");  // warps per task (1 = warp-per-task kernel)
+    const char* e = std::getenv("KVX_MATCH_GROUP");  // 1 = the warp-per-task kernel
+    const int v = e ? std::atoi(e) : 2;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 2;
+  }();
+  static const int chains = [] {
+    const char* e = std::getenv("KVX_MATCH_CHAINS");
     const int v = e ? std::atoi(e) : 4;
-    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 4;
+    return v == 1 || v == 2 || v == 4 ? v : 4;
   }();
   if (group > 1) {
     const int64_t cap = static_cast<int64_t>(sm_count(dev)) * (64 / group);  // 2048 threads / SM
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(tasks, cap)));
-    switch (group) {
-      case 2:
-        match_group_kernel<2><<<blocks, 64, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out,
-                                                    d_best_len, d_best_id);
-        break;
-      case 8:
-        match_group_kernel<8><<<blocks, 256, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out,
-                                                     d_best_len, d_best_id);
-        break;
-      default:
-        match_group_kernel<4><<<blocks, 128, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out,
-                                                     d_best_len, d_best_id);
+    const int threads = 32 * group;
+#define KVX_MATCH_G(G, C)                                                                  \
+  match_group_kernel<G, C><<<blocks, threads, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out, \
+                                                      d_best_len, d_best_id)
+    switch (group * 10 + chains) {
+      case 21: KVX_MATCH_G(2, 1); break;
+      case 22: KVX_MATCH_G(2, 2); break;
+      case 41: KVX_MATCH_G(4, 1); break;
+      case 42: KVX_MATCH_G(4, 2); break;
+      case 44: KVX_MATCH_G(4, 4); break;
+      case 81: KVX_MATCH_G(8, 1); break;
+      case 82: KVX_MATCH_G(8, 2); break;
+      case 84: KVX_MATCH_G(8, 4); break;
+      default: KVX_MATCH_G(2, 4);
     }
+#undef KVX_MATCH_G
     KVX_LAUNCH_CHECK("match_group_kernel");
   } else {
   const int threads = 256;
