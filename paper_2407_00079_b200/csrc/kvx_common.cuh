@@ -76,12 +76,14 @@ int copy_paged_overlapped(const kvx_pool* src, const int32_t* d_src_table, kvx_p
 // PEER_PULL receiver pieces (kvx_copy.cu): a one-warp gate that waits for the
 // sender's flag (d_flag >= value, system-scope acquire; 20 s timeout sets
 // *d_status), the pull copy (after_gate: programmatically dependent on the
-// gate, skips when *d_status != 0), and the end-of-step "consumed" word.
+// gate; re-acquires the flag, skips when *d_status != 0), and the end-of-step
+// "consumed" word.
 int pull_gate(const uint64_t* d_flag, uint64_t value, uint64_t* d_status, void* stream,
               bool overlap_prev);
 int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
                     const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, void* stream,
-                    const uint64_t* d_status, bool after_gate);
+                    const uint64_t* d_flag, uint64_t value, const uint64_t* d_status,
+                    bool after_gate);
 int pull_done(const uint64_t* d_status, uint64_t* d_peer_flag, uint64_t value, void* stream);
 
 }  // namespace kvx

@@ -251,15 +251,35 @@ __global__ void __launch_bounds__(32) pull_gate_kernel(const unsigned long long*
 
 // The pull copy: coherent loads of the peer pool (another GPU wrote it while
 // this grid may already have been launched), evict-first local stores.  It
-// first waits for its gate to complete (griddepcontrol.wait: no-op for a plain
-// launch) and then lets the next unit's gate be scheduled.
+// is launched (programmatically dependent on its gate) only once the gate saw
+// the unit's flag, so thread 0's own system-scope acquire of the flag passes
+// at once and orders the CTA's loads after the sender's writes (the CTA
+// barrier carries it); it does NOT wait for the gate grid to complete, which
+// would serialise it behind the previous unit's copy.  A gate that timed out
+// raised *status: the copy then skips.  Then the next unit's gate may be
+// scheduled.
 template <class Idx>
 __global__ void __launch_bounds__(kLsuThreads, 2) copy_pull_kernel(
-    const SlabCopy c, const unsigned long long* __restrict__ status) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+    const SlabCopy c, const unsigned long long* __restrict__ flag, unsigned long long value,
+    const unsigned long long* __restrict__ status) {
+  __shared__ int go;
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    while (true) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      if (v >= value) break;
+      if (*reinterpret_cast<const volatile unsigned long long*>(status)) {
+        ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+    go = ok;
+  }
+  __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (status && *reinterpret_cast<const volatile unsigned long long*>(status)) return;
-  lsu_copy<true, true, Idx, true>(c);
+  if (go) lsu_copy<true, true, Idx, true>(c);
 }
 
 // Receiver -> sender "source blocks consumed" word of a PEER_PULL step: the
@@ -806,7 +826,8 @@ int pull_done(const uint64_t* d_status, uint64_t* d_peer_flag, uint64_t value, v
 
 int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* dst,
                     const int32_t* d_dst_table, int64_t n, int32_t lo, int32_t hi, void* stream,
-                    const uint64_t* d_status, bool after_gate) {
+                    const uint64_t* d_flag, uint64_t value, const uint64_t* d_status,
+                    bool after_gate) {
   SlabCopy c;
   bool empty = false;
   const int st = paged_copy_args(src, d_src_table, dst, d_dst_table, n, lo, hi, &c, &empty);
@@ -822,11 +843,14 @@ int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* d
   cudaLaunchAttribute attr[1] = {pdl_attr()};
   cfg.attrs = after_gate ? attr : nullptr;
   cfg.numAttrs = after_gate ? 1 : 0;
-  const auto* f = reinterpret_cast<const unsigned long long*>(d_status);
+  KVX_REQUIRE(d_flag && d_status, "copy_paged_pull: NULL flag or status");
+  const auto* fl = reinterpret_cast<const unsigned long long*>(d_flag);
+  const auto* stw = reinterpret_cast<const unsigned long long*>(d_status);
+  const unsigned long long v = value;
   if (items + blocks < (int64_t{1} << 32))
-    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<uint32_t>, c, f));
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<uint32_t>, c, fl, v, stw));
   else
-    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<int64_t>, c, f));
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, copy_pull_kernel<int64_t>, c, fl, v, stw));
   KVX_LAUNCH_CHECK("copy_pull_kernel");
   return KVX_OK;
 }

@@ -776,8 +776,8 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
   }();
   static const int chains = [] {
     const char* e = std::getenv("KVX_MATCH_CHAINS");
-    const int v = e ? std::atoi(e) : 4;
-    return v == 1 || v == 2 || v == 4 ? v : 4;
+    const int v = e ? std::atoi(e) : 2;
+    return v == 1 || v == 2 || v == 4 ? v : 2;
   }();
   if (group > 1) {
     const int64_t cap = static_cast<int64_t>(sm_count(dev)) * (64 / group);  // 2048 threads / SM
@@ -788,14 +788,14 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
                                                       d_best_len, d_best_id)
     switch (group * 10 + chains) {
       case 21: KVX_MATCH_G(2, 1); break;
-      case 22: KVX_MATCH_G(2, 2); break;
       case 41: KVX_MATCH_G(4, 1); break;
       case 42: KVX_MATCH_G(4, 2); break;
       case 44: KVX_MATCH_G(4, 4); break;
       case 81: KVX_MATCH_G(8, 1); break;
       case 82: KVX_MATCH_G(8, 2); break;
       case 84: KVX_MATCH_G(8, 4); break;
-      default: KVX_MATCH_G(2, 4);
+      case 24: KVX_MATCH_G(2, 4); break;
+      default: KVX_MATCH_G(2, 2);
     }
 #undef KVX_MATCH_G
     KVX_LAUNCH_CHECK("match_group_kernel");

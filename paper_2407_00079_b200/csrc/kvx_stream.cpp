@@ -57,7 +57,7 @@ struct kvx_streamer {
   uint64_t* flag = nullptr;          // local 64-bit flag word (peer writes it)
   uint64_t* pull_status = nullptr;   // PEER_PULL receiver: nonzero once a unit's gate timed out
   bool same_gpu = false;             // the peer process runs on this very GPU
-  bool gate_kernel = false;          // PEER_PULL receiver: units released by the gate kernel
+  int pull_wait = 0;                 // PEER_PULL receiver: kPullGate / kPullInline / kPullStream
   uint64_t* peer_flag = nullptr;     // the peer's flag word, mapped here
   kvx_pool* peer_view = nullptr;     // PEER_FUSED: receiver's pool as seen by the sender
   uint64_t seq = 0;                  // units issued (sender) / consumed (receiver)
@@ -135,14 +135,27 @@ int device_uuid(int dev, uint8_t out[16]) {
   return KVX_OK;
 }
 
-// KVX_PULL_GATE=stream: release PEER_PULL units with stream waits instead of
-// the gate kernel (measurement knob; always so when both ends share a GPU).
-bool pull_gate_kernel_enabled() {
-  static const bool on = [] {
+// How a PEER_PULL receiver waits for the sender's unit flag:
+//   kPullGate   (default) a one-warp gate kernel waits; the copy launches
+//               programmatically dependent on it (only the gate is resident
+//               while the data is not there)
+//   kPullInline the copy itself waits (thread 0 of every CTA), launched
+//               programmatically dependent on the previous unit's copy: the
+//               r01 design -- the next unit's whole grid sits resident while
+//               the sender has not produced it
+//   kPullStream the stream front end waits (cuStreamWaitValue64); the copy is
+//               a plain launch
+// KVX_PULL_GATE=gate|inline|stream selects it (measurement knob); two
+// processes sharing one GPU always use kPullStream.
+enum { kPullGate = 0, kPullInline = 1, kPullStream = 2 };
+int pull_wait_mode() {
+  static const int m = [] {
     const char* e = std::getenv("KVX_PULL_GATE");
-    return !(e && std::strcmp(e, "stream") == 0);
+    if (e && std::strcmp(e, "stream") == 0) return static_cast<int>(kPullStream);
+    if (e && std::strcmp(e, "inline") == 0) return static_cast<int>(kPullInline);
+    return static_cast<int>(kPullGate);
   }();
-  return on;
+  return m;
 }
 
 bool is_peer(const kvx_streamer* s) {
@@ -310,7 +323,7 @@ int kvx_streamer_connect(kvx_streamer* s, const uint8_t* blob, int64_t len,
   int rc = device_uuid(s->device, mine);
   if (rc) return rc;
   s->same_gpu = std::memcmp(mine, b.uuid, 16) == 0;
-  s->gate_kernel = !s->same_gpu && pull_gate_kernel_enabled();
+  s->pull_wait = s->same_gpu ? kPullStream : pull_wait_mode();
   void* p = nullptr;
   rc = kvx_ipc_open(b.flag, s->device, &p);
   if (rc) return rc;
@@ -478,11 +491,14 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t
         const bool sampled = will_sample(s);
         const bool pdl = pdl_enabled();
         int rc = KVX_OK;
-        bool after_gate = false;
-        if (s->gate_kernel) {
+        bool after_gate = false;  // launch the copy programmatically dependent
+        if (s->pull_wait == kPullGate) {
           rc = kvx::pull_gate(s->flag, c + 1, s->pull_status, s->s_main,
                               pdl && !first_unit && !sampled);
           after_gate = pdl && !sampled;
+        } else if (s->pull_wait == kPullInline) {
+          after_gate = pdl && !first_unit && !sampled;  // on the previous unit's copy
+          if (first_unit || sampled) rc = kvx_signal_wait(s->s_main, s->flag, c + 1);
         } else {
           rc = kvx_signal_wait(s->s_main, s->flag, c + 1);
         }
@@ -490,7 +506,8 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t
         if (rc) return rc;
         rc = timed_launch(s, s->s_main, 1.0 * payload, [&] {
           return kvx::copy_paged_pull(s->peer_view, d_src_table + b0, s->dst, d_dst_table + b0, nb,
-                                      l0, l1, s->s_main, s->pull_status, after_gate);
+                                      l0, l1, s->s_main, s->flag, c + 1, s->pull_status,
+                                      after_gate);
         });
         if (rc) return rc;
         continue;
