@@ -51,29 +51,31 @@ dst_t = torch.as_tensor(rng.permutation(slots)[:n].astype(np.int32), device=d)
 cycles = int(args.delay_us * 1e-6 * 1.9e9)
 
 
-def gemm_rate(stream, stop_event=None, iters=None):
-    """bf16 GEMM loop on `stream`: until stop_event completes (polled from the
-    host) or for `iters` launches; returns TFLOP/s by CUDA events."""
-    a = torch.randn(8192, 8192, dtype=torch.bfloat16, device=d)
-    b = torch.randn(8192, 8192, dtype=torch.bfloat16, device=d)
-    c = torch.empty(8192, 8192, dtype=torch.bfloat16, device=d)
+A = B = C_ = None
+
+
+def gemm_rate(stream, iters=20):
+    """`iters` back-to-back bf16 8192^3 GEMMs on `stream`; TFLOP/s by CUDA
+    events around the whole loop (enqueued at once: they run as soon as the
+    SMs let them)."""
+    global A, B, C_
+    if A is None:
+        A = torch.randn(8192, 8192, dtype=torch.bfloat16, device=d)
+        B = torch.randn(8192, 8192, dtype=torch.bfloat16, device=d)
+        C_ = torch.empty(8192, 8192, dtype=torch.bfloat16, device=d)
+        torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k = 0
     with torch.cuda.stream(stream):
-        torch.matmul(a, b, out=c)
         e0.record(stream)
-        while True:
-            torch.matmul(a, b, out=c)
-            k += 1
-            if iters and k >= iters:
-                break
-            if stop_event is not None and k % 4 == 0 and stop_event.query():
-                break
-            if stop_event is not None and k > 400:
-                break
+        for _ in range(iters):
+            torch.matmul(A, B, out=C_)
         e1.record(stream)
-    e1.synchronize()
-    return 2 * 8192 ** 3 * k / (e0.elapsed_time(e1) / 1e3) / 1e12, k
+    return e0, e1, iters
+
+
+def rate(ev):
+    e0, e1, k = ev
+    return 2 * 8192 ** 3 * k / (e0.elapsed_time(e1) / 1e3) / 1e12
 
 
 def one_step(with_gemm):
@@ -89,14 +91,18 @@ def one_step(with_gemm):
         st.finish(torch.cuda.current_stream())
         torch.cuda.synchronize()
     else:
+        gs = torch.cuda.Stream(rank)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         st.recv(dst_t, 0, L, 0, 1, src_table=src_t)
         e1.record(s)
         st.finish(torch.cuda.current_stream())
-        if with_gemm:
-            res["gemm_tflops"], res["gemm_iters"] = gemm_rate(torch.cuda.Stream(rank), e1)
+        g = gemm_rate(gs) if with_gemm else None  # ~14 ms of GEMMs inside the ~16 ms transfer
         torch.cuda.synchronize()
+        if g is not None:
+            res["gemm_tflops_during_transfer"] = rate(g)
+            res["gemm_window_ms"] = g[0].elapsed_time(g[1])
+            res["gemm_started_after_transfer_start_ms"] = e0.elapsed_time(g[0])
         st.check()
         res["transfer_ms"] = e0.elapsed_time(e1)
         bad = torch.zeros(1, dtype=torch.int64, device=d)
@@ -110,7 +116,9 @@ def one_step(with_gemm):
 one_step(False)
 alone = None
 if role.role == "decode":
-    alone, _ = gemm_rate(torch.cuda.Stream(rank), iters=40)
+    ev = gemm_rate(torch.cuda.Stream(rank))
+    torch.cuda.synchronize()
+    alone = rate(ev)
 dist.barrier()
 r = one_step(True)
 if role.role == "decode":
