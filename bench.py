@@ -1149,14 +1149,15 @@ def bench_match_sharded(args, dev, rank, world, s, o):
 def bench_host_tier(args, dev):
     """CPU-DRAM tier (a12): one LLaMA2-70B request of 8K tokens whose first
     half (256 blocks, Config 2's shared prefix) is cached in DRAM.  Measured:
-    the copy-engine PCIe peaks (1 GiB pinned H2D / D2H), the layer-wise load of
-    the prefix DRAM -> HBM and store of the fresh half HBM -> DRAM (copy
-    kernels of host_copy_ctas CTAs over PCIe), and a layer-wise prefill with
-    Mooncake's launch / wait per layer: per layer, wait for the
-    layer's load, run that layer's compute (a bf16 GEMM standing in for the
-    layer: 4096 x 8192 x 8192), launch the layer's store; the reference models
-    it as max(compute, load) (layerwise_effective_prefill,
-    proj/src/perf_model.cpp:73-85)."""
+    the copy-engine PCIe peaks (1 GiB pinned H2D / D2H); the layer-wise load
+    of the prefix DRAM -> HBM and store of the fresh half HBM -> DRAM, for
+    scattered blocks (copy kernels of host_copy_ctas CTAs over PCIe) and for
+    contiguous block runs (two copy-engine copies per layer); and a
+    layer-wise prefill with Mooncake's launch / wait per layer:
+    per layer, wait for the layer's load, run that layer's compute (a bf16
+    GEMM standing in for the layer: 4096 x 8192 x 8192), launch the layer's
+    store.  The reference models it as max(compute, load)
+    (layerwise_effective_prefill, proj/src/perf_model.cpp:73-85)."""
     import torch
 
     import paper_2407_00079_b200 as pkg
@@ -1172,6 +1173,8 @@ def bench_host_tier(args, dev):
     dt = torch.as_tensor(rng.permutation(1024)[: n_pre + n_new].astype(np.int32), device=d)
     h_pre, d_pre = ht[:n_pre], dt[:n_pre]
     h_new, d_new = ht[n_pre:], dt[n_pre:]
+    # contiguous runs: DRAM slots [1024, 1280) / [1280, 1536), HBM [512, 768) / [768, 1024)
+    ch_pre, cd_pre, ch_new, cd_new = 1024, 512, 1280, 768
     slab = hbm.slab
     load_bytes = L * 2 * n_pre * slab
     store_bytes = L * 2 * n_new * slab
@@ -1181,7 +1184,7 @@ def bench_host_tier(args, dev):
     def ev():
         return torch.cuda.Event(enable_timing=True)
 
-    # copy-engine PCIe peaks (pinned host memory, 1 GiB, best of 3)
+    # copy-engine PCIe peaks (pinned host memory, 1 GiB, best of 4)
     nb = 1 << 30
     pin = torch.empty(nb, dtype=torch.uint8).pin_memory()
     gbuf = torch.empty(nb, dtype=torch.uint8, device=d)
@@ -1211,28 +1214,22 @@ def bench_host_tier(args, dev):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
-    def load_all():
-        io.load(host, h_pre, hbm, d_pre, 0, L, after=s)
-        io.wait_layer(L - 1, s)
+    def load(contig):
+        if contig:
+            io.load_range(host, ch_pre, hbm, cd_pre, n_pre, 0, L, after=s)
+        else:
+            io.load(host, h_pre, hbm, d_pre, 0, L, after=s)
 
-    def store_all():
-        io.store(hbm, d_new, host, h_new, 0, L, after=s)
-        io.wait_stores(s)
+    def store(contig, layer_lo, layer_hi):
+        if contig:
+            io.store_range(hbm, cd_new, host, ch_new, n_new, layer_lo, layer_hi, after=s)
+        else:
+            io.store(hbm, d_new, host, h_new, layer_lo, layer_hi, after=s)
 
     reps = max(3, min(args.steps, 10))
-    load_ms = timed(load_all, reps)
     bad = torch.zeros(1, dtype=torch.int64, device=d)
-    hbm.verify(d_pre, 7, h_pre, 0, L, counter=bad, stream=s)
-    s.synchronize()
-    assert bad.item() == 0, "DRAM-tier load parity"
-    with torch.cuda.stream(s):
-        hbm.fill_synthetic(8, stream=s)
-    store_ms = timed(store_all, reps)
-    host.verify(h_new, 8, d_new, 0, L, counter=bad, stream=s)
-    s.synchronize()
-    assert bad.item() == 0, "DRAM-tier store parity"
-
-    # layer-wise prefill: launch / wait per layer around a per-layer GEMM
+    ar = torch.arange
+    res = {}
     with torch.cuda.stream(s):
         x = torch.randn(4096, 8192, dtype=torch.bfloat16, device=d)
         w = torch.randn(8192, 8192, dtype=torch.bfloat16, device=d)
@@ -1243,35 +1240,70 @@ def bench_host_tier(args, dev):
             for _ in range(L):
                 torch.matmul(x, w, out=y)
 
-    def layerwise():
-        io.load(host, h_pre, hbm, d_pre, 0, L, after=s)   # launch every layer's load
-        with torch.cuda.stream(s):
-            for layer in range(L):
-                io.wait_layer(layer, s)                   # wait before the layer's attention
-                torch.matmul(x, w, out=y)
-                io.store(hbm, d_new, host, h_new, layer, layer + 1, after=s)  # launch its store
-        io.wait_stores(s)                                 # all stores at the end
-
     compute_ms = timed(compute_only, reps)
-    lw_ms = timed(layerwise, reps)
+    for contig in (False, True):
+        def load_all():
+            load(contig)
+            io.wait_layer(L - 1, s)
+
+        def store_all():
+            store(contig, 0, L)
+            io.wait_stores(s)
+
+        def layerwise():
+            load(contig)                                   # launch every layer's load
+            with torch.cuda.stream(s):
+                for layer in range(L):
+                    io.wait_layer(layer, s)                # wait before the layer's attention
+                    torch.matmul(x, w, out=y)
+                    store(contig, layer, layer + 1)        # launch the layer's store
+            io.wait_stores(s)                              # all stores at the end
+
+        load_ms = timed(load_all, reps)
+        # parity of the load: every loaded word against the synthetic DRAM content
+        if contig:
+            hbm.verify(ar(cd_pre, cd_pre + n_pre, dtype=torch.int32, device=d), 7,
+                       ar(ch_pre, ch_pre + n_pre, dtype=torch.int32, device=d), 0, L,
+                       counter=bad, stream=s)
+        else:
+            hbm.verify(d_pre, 7, h_pre, 0, L, counter=bad, stream=s)
+        s.synchronize()
+        assert bad.item() == 0, "DRAM-tier load parity"
+        with torch.cuda.stream(s):
+            hbm.fill_synthetic(8, stream=s)
+        store_ms = timed(store_all, reps)
+        if contig:
+            host.verify(ar(ch_new, ch_new + n_new, dtype=torch.int32, device=d), 8,
+                        ar(cd_new, cd_new + n_new, dtype=torch.int32, device=d), 0, L,
+                        counter=bad, stream=s)
+        else:
+            host.verify(h_new, 8, d_new, 0, L, counter=bad, stream=s)
+        s.synchronize()
+        assert bad.item() == 0, "DRAM-tier store parity"
+        lw_ms = timed(layerwise, reps)
+        res["contiguous_copy_engine" if contig else "paged_sm_copy"] = {
+            "load": {"bytes": load_bytes, "ms": load_ms, "gbs": load_bytes / (load_ms / 1e3) / GB,
+                     "frac_of_h2d_peak": load_bytes / (load_ms / 1e3) / GB / h2d_peak},
+            "store": {"bytes": store_bytes, "ms": store_ms,
+                      "gbs": store_bytes / (store_ms / 1e3) / GB,
+                      "frac_of_d2h_peak": store_bytes / (store_ms / 1e3) / GB / d2h_peak},
+            "layerwise_prefill": {
+                "compute_ms": compute_ms, "load_ms": load_ms, "store_ms": store_ms,
+                "measured_ms": lw_ms, "model_ms": max(compute_ms, load_ms),
+                "overlap_efficiency": max(compute_ms, load_ms) / lw_ms},
+            "how": ("two copy-engine copies per layer (contiguous block runs), no kernel" if contig
+                    else "one copy kernel per layer, grid capped for PCIe (KVX_HOST_COPY_CTAS, "
+                         "default 16), scattered blocks via block tables")}
     return {
         "metric": "layer-wise DRAM <-> HBM KV load / store GB/s (CPU-DRAM tier)",
         "workload": "one 8K-token LLaMA2-70B request: 256-block prefix cached in DRAM (load), "
                     "256 fresh blocks stored back (bs 16, fp16, 80 layers)",
-        "load": {"bytes": load_bytes, "ms": load_ms, "gbs": load_bytes / (load_ms / 1e3) / GB,
-                 "frac_of_h2d_peak": load_bytes / (load_ms / 1e3) / GB / h2d_peak},
-        "store": {"bytes": store_bytes, "ms": store_ms,
-                  "gbs": store_bytes / (store_ms / 1e3) / GB,
-                  "frac_of_d2h_peak": store_bytes / (store_ms / 1e3) / GB / d2h_peak},
+        **res,
         "pcie_peak": {"h2d_gbs": h2d_peak, "d2h_gbs": d2h_peak,
                       "how": "copy engine, 1 GiB pinned, best of 4, measured in this run"},
-        "kernel": "copy_lsu_kernel, grid capped for PCIe (KVX_HOST_COPY_CTAS, default 16)",
-        "layerwise_prefill": {
-            "compute_ms": compute_ms, "load_ms": load_ms, "store_ms": store_ms,
-            "measured_ms": lw_ms, "model_ms": max(compute_ms, load_ms),
-            "model": "layerwise_effective_prefill = max(compute, cache load) "
-                     "(proj/src/perf_model.cpp:73-78)",
-            "compute": "per layer one bf16 GEMM 4096x8192x8192 (stand-in for the layer)"},
+        "model": "layerwise_effective_prefill = max(compute, cache load) "
+                 "(proj/src/perf_model.cpp:73-78); compute = per layer one bf16 GEMM "
+                 "4096x8192x8192 (stand-in for the layer)",
         "parity": "every loaded / stored word verified against the synthetic source",
     }
 

@@ -431,6 +431,17 @@ int kvx_layer_store_launch(kvx_layer_io* io, const kvx_pool* dev, const int32_t*
                            kvx_pool* host, const int32_t* d_host_table, int64_t n,
                            int32_t layer_lo, int32_t layer_hi, void* after_stream);
 int kvx_layer_store_wait_all(kvx_layer_io* io, void* stream);
+/* The same for CONTIGUOUS block runs: host slots [host_first, host_first+n)
+ * <-> device slots [dev_first, dev_first+n).  Each (layer, K|V) plane is then
+ * one contiguous range on both sides: two copy-engine copies per layer and
+ * no kernel, so the SMs stay with the prefill (a register-heavy GEMM leaves
+ * no room for a copy kernel to run beside it). */
+int kvx_layer_load_range(kvx_layer_io* io, const kvx_pool* host, int64_t host_first,
+                         kvx_pool* dev, int64_t dev_first, int64_t n, int32_t layer_lo,
+                         int32_t layer_hi, void* after_stream);
+int kvx_layer_store_range(kvx_layer_io* io, const kvx_pool* dev, int64_t dev_first,
+                          kvx_pool* host, int64_t host_first, int64_t n, int32_t layer_lo,
+                          int32_t layer_hi, void* after_stream);
 
 /* ---- KVCache store of one instance + migration (hot-spot replication) ---- */
 

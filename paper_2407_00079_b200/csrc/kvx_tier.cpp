@@ -8,11 +8,14 @@
 // kv_bytes_per_token / load_bandwidth (cache_load_time, perf_model.cpp:80-85;
 // load_bandwidth preset 30 GB/s, proj/src/config.cpp:218).  Here the bytes
 // really move: the DRAM pool is pinned, device-mapped host memory in the same
-// paged layout as HBM, and each layer is ONE copy kernel with a small grid
-// (host_copy_ctas) that reads / writes it over PCIe -- paged slabs need no
-// staging, and the other SMs stay free for the prefill compute.  Loads and
-// stores each have their own in-order queue, so a layer's load overlaps the
-// previous layer's attention and its store overlaps the next layer's.
+// paged layout as HBM.  Scattered blocks: each layer is ONE copy kernel with a
+// small grid (host_copy_ctas) that reads / writes it over PCIe, no staging.
+// Contiguous block runs (kvx_layer_*_range): two copy-engine copies per
+// layer and no kernel, so the SMs stay entirely with the prefill (a
+// register-heavy GEMM leaves no room for a copy kernel beside it: bench.py's
+// host_tier object measures both).  Loads and stores each have their own
+// in-order queue, so a layer's load overlaps the previous layer's attention
+// and its store overlaps the next layer's.
 #include <cuda_runtime.h>
 
 #include <vector>
@@ -122,6 +125,74 @@ int kvx_layer_store_launch(kvx_layer_io* io, const kvx_pool* dev, const int32_t*
   if (rc) return rc;
   for (int32_t l = layer_lo; l < layer_hi; ++l) {
     rc = kvx_copy_paged(dev, d_dev_table, host, d_host_table, n, l, l + 1, io->store_q);
+    if (rc) return rc;
+  }
+  return KVX_OK;
+}
+
+// Contiguous runs (the block range [h0, h0+n) of the DRAM pool <-> [d0, d0+n)
+// of the HBM pool): each (layer, K|V) plane is then ONE contiguous range on
+// both sides, so a layer is two copy-engine copies and no kernel -- the SMs
+// stay entirely with the prefill compute, which register-heavy GEMMs would
+// not leave to a copy kernel anyway.
+namespace {
+int range_copy(kvx_layer_io* io, cudaStream_t q, const kvx_pool* from, int64_t f0, kvx_pool* to,
+               int64_t t0, int64_t n, int32_t l) {
+  const int64_t slab = kvx_pool_slab_bytes(from);
+  const int64_t fslots = kvx_pool_bytes(from) / (2 * kvx_pool_layers(from) * slab);
+  const int64_t tslots = kvx_pool_bytes(to) / (2 * kvx_pool_layers(to) * slab);
+  KVX_REQUIRE(f0 >= 0 && t0 >= 0 && n >= 0 && f0 + n <= fslots && t0 + n <= tslots,
+              "kvx_layer_*_range: block range outside a pool");
+  auto* fb = static_cast<const uint8_t*>(kvx_pool_base(from));
+  auto* tb = static_cast<uint8_t*>(kvx_pool_base(to));
+  for (int kv = 0; kv < 2; ++kv) {
+    const int64_t fp = ((static_cast<int64_t>(l) * 2 + kv) * fslots + f0) * slab;
+    const int64_t tp = ((static_cast<int64_t>(l) * 2 + kv) * tslots + t0) * slab;
+    if (n) KVX_CUDA(cudaMemcpyAsync(tb + tp, fb + fp, static_cast<size_t>(n * slab),
+                                    cudaMemcpyDefault, q));
+  }
+  return KVX_OK;
+}
+}  // namespace
+
+int kvx_layer_load_range(kvx_layer_io* io, const kvx_pool* host, int64_t host_first,
+                         kvx_pool* dev, int64_t dev_first, int64_t n, int32_t layer_lo,
+                         int32_t layer_hi, void* after_stream) {
+  KVX_REQUIRE(io && host && dev, "kvx_layer_load_range: NULL argument");
+  KVX_REQUIRE(kvx_pool_is_host(host) && !kvx_pool_is_host(dev),
+              "kvx_layer_load_range: loads go from a host (DRAM) pool into a device pool");
+  KVX_REQUIRE(kvx_pool_slab_bytes(host) == kvx_pool_slab_bytes(dev),
+              "kvx_layer_load_range: pools have different block shapes");
+  KVX_REQUIRE(0 <= layer_lo && layer_lo <= layer_hi && layer_hi <= io->max_layers &&
+                  layer_hi <= kvx_pool_layers(host) && layer_hi <= kvx_pool_layers(dev),
+              "kvx_layer_load_range: bad layer range");
+  kvx::DeviceGuard g(io->device);
+  int rc = order_after(io, io->load_q, after_stream);
+  if (rc) return rc;
+  for (int32_t l = layer_lo; l < layer_hi; ++l) {
+    rc = range_copy(io, io->load_q, host, host_first, dev, dev_first, n, l);
+    if (rc) return rc;
+    KVX_CUDA(cudaEventRecord(io->loaded[l], io->load_q));
+  }
+  return KVX_OK;
+}
+
+int kvx_layer_store_range(kvx_layer_io* io, const kvx_pool* dev, int64_t dev_first,
+                          kvx_pool* host, int64_t host_first, int64_t n, int32_t layer_lo,
+                          int32_t layer_hi, void* after_stream) {
+  KVX_REQUIRE(io && host && dev, "kvx_layer_store_range: NULL argument");
+  KVX_REQUIRE(kvx_pool_is_host(host) && !kvx_pool_is_host(dev),
+              "kvx_layer_store_range: stores go from a device pool into a host (DRAM) pool");
+  KVX_REQUIRE(kvx_pool_slab_bytes(host) == kvx_pool_slab_bytes(dev),
+              "kvx_layer_store_range: pools have different block shapes");
+  KVX_REQUIRE(0 <= layer_lo && layer_lo <= layer_hi && layer_hi <= io->max_layers &&
+                  layer_hi <= kvx_pool_layers(host) && layer_hi <= kvx_pool_layers(dev),
+              "kvx_layer_store_range: bad layer range");
+  kvx::DeviceGuard g(io->device);
+  int rc = order_after(io, io->store_q, after_stream);
+  if (rc) return rc;
+  for (int32_t l = layer_lo; l < layer_hi; ++l) {
+    rc = range_copy(io, io->store_q, dev, dev_first, host, host_first, n, l);
     if (rc) return rc;
   }
   return KVX_OK;

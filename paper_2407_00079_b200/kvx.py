@@ -126,6 +126,8 @@ _sig("kvx_layer_load_launch", C.c_int, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32
 _sig("kvx_layer_load_wait", C.c_int, _vp, _i32, _vp)
 _sig("kvx_layer_store_launch", C.c_int, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp)
 _sig("kvx_layer_store_wait_all", C.c_int, _vp, _vp)
+_sig("kvx_layer_load_range", C.c_int, _vp, _vp, _i64, _vp, _i64, _i64, _i32, _i32, _vp)
+_sig("kvx_layer_store_range", C.c_int, _vp, _vp, _i64, _vp, _i64, _i64, _i32, _i32, _vp)
 _sig("kvx_pool_destroy", C.c_int, _vp)
 _sig("kvx_pool_base", _vp, _vp)
 _sig("kvx_pool_slab_bytes", _i64, _vp)
@@ -615,6 +617,17 @@ class LayerIO:
         check(_L.kvx_layer_store_launch(self.h, dev.h, _ptr(dev_table), host.h, _ptr(host_table),
                                         dev_table.numel(), layer_lo, layer_hi,
                                         _stream(after) if after is not None else None))
+
+    def load_range(self, host: "KVPool", host_first: int, dev: "KVPool", dev_first: int, n: int,
+                   layer_lo: int, layer_hi: int, after=None):
+        """Contiguous runs: two copy-engine copies per layer, no kernel."""
+        check(_L.kvx_layer_load_range(self.h, host.h, host_first, dev.h, dev_first, n, layer_lo,
+                                      layer_hi, _stream(after) if after is not None else None))
+
+    def store_range(self, dev: "KVPool", dev_first: int, host: "KVPool", host_first: int, n: int,
+                    layer_lo: int, layer_hi: int, after=None):
+        check(_L.kvx_layer_store_range(self.h, dev.h, dev_first, host.h, host_first, n, layer_lo,
+                                       layer_hi, _stream(after) if after is not None else None))
 
     def wait_stores(self, stream=None):
         """stream None: host-blocking."""

@@ -15,3 +15,10 @@ for N in 2 4; do
     echo "n$N c$c rc=$?"
   done
 done
+# decode-GPU starvation while a pull receiver waits for a slow prefill (2 of the GPUs)
+for M in gate inline stream; do
+  P=$((P+1))
+  KVX_PULL_GATE=$M timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+    --master-addr 127.0.0.1 --master-port $P tests/perf/pull_starvation.py 2>&1 | grep '^{' \
+    | tee -a gpurun_out/$T/pull_starvation.txt
+done

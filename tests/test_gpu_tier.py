@@ -94,3 +94,32 @@ def test_layer_io_validation(kvx):
         io.load(host, t, dev, t, 0, 3)  # past max_layers
     with pytest.raises(kvx.ValidationError):
         io.store(host, t, dev, t, 0, 1)
+
+
+def test_contiguous_range_load_store_vs_oracle(kvx, oracle_lib):
+    """Contiguous block runs move by copy engine (kvx_layer_*_range): the
+    same bytes as the paged copy of the equivalent ascending tables."""
+    L, hs, ds, n = 5, 60, 50, 17
+    host, dev = _pools(kvx, L, 16, 2, hs, ds)
+    host.fill_synthetic(6)
+    dev.tensor_view().zero_()
+    io = kvx.LayerIO(0, L)
+    s = torch.cuda.Stream(0)
+    io.load_range(host, 31, dev, 9, n, 1, L, after=s)  # layers [1, L)
+    io.wait_layer(L - 1, s)
+    s.synchronize()
+    torch.cuda.synchronize()
+    want = np.zeros(dev.nbytes, dtype=np.uint8)
+    oracle_lib.copy_paged(host.host_array().copy(), hs, np.arange(31, 31 + n, dtype=np.int32),
+                          want, ds, np.arange(9, 9 + n, dtype=np.int32), dev.slab, 1, L)
+    assert np.array_equal(dev.tensor_view().cpu().numpy(), want)
+    back = kvx.KVPool(L, 16, 8, 128, 2, hs, 0, host=True)
+    back.host_array()[:] = 0
+    io.store_range(dev, 9, back, 0, n, 0, L, after=s)
+    io.wait_stores()
+    want2 = np.zeros(back.nbytes, dtype=np.uint8)
+    oracle_lib.copy_paged(want, ds, np.arange(9, 9 + n, dtype=np.int32), want2, hs,
+                          np.arange(0, n, dtype=np.int32), dev.slab, 0, L)
+    assert np.array_equal(back.host_array(), want2)
+    with pytest.raises(kvx.ValidationError):
+        io.load_range(host, hs - 3, dev, 0, 4, 0, 1)  # past the DRAM pool
