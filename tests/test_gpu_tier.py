@@ -35,6 +35,7 @@ def test_layerwise_load_store_vs_oracle(kvx, oracle_lib, bs, db):
     host, dev = _pools(kvx, L, bs, db, hs, ds)
     host.fill_synthetic(2)
     dev.tensor_view().zero_()
+    torch.cuda.synchronize()  # the fill / zero run on the current stream, the loads on io's
     rng = np.random.default_rng(bs)
     ht = rng.permutation(hs)[:n].astype(np.int32)
     dt = rng.permutation(ds)[:n].astype(np.int32)
@@ -103,6 +104,7 @@ def test_contiguous_range_load_store_vs_oracle(kvx, oracle_lib):
     host, dev = _pools(kvx, L, 16, 2, hs, ds)
     host.fill_synthetic(6)
     dev.tensor_view().zero_()
+    torch.cuda.synchronize()
     io = kvx.LayerIO(0, L)
     s = torch.cuda.Stream(0)
     io.load_range(host, 31, dev, 9, n, 1, L, after=s)  # layers [1, L)
