@@ -1168,6 +1168,7 @@ def bench_host_tier(args, dev):
     host = pkg.KVPool(L, bs, 8, 128, args.dtype_bytes, host_slots, dev, host=True)
     hbm = pkg.KVPool(L, bs, 8, 128, args.dtype_bytes, 1024, dev)
     host.fill_synthetic(7)
+    torch.cuda.synchronize()  # the fill runs on the current stream, the loads on io's queue
     rng = np.random.default_rng(12)
     ht = torch.as_tensor(rng.permutation(host_slots)[: n_pre + n_new].astype(np.int32), device=d)
     dt = torch.as_tensor(rng.permutation(1024)[: n_pre + n_new].astype(np.int32), device=d)

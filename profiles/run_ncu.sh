@@ -4,8 +4,8 @@
 # Outputs land in gpurun_out/; summaries go to profiles/ via summarize_ncu.py.
 set -e
 mkdir -p gpurun_out
-SMALL="--requests 16 --wave 16 --steps 2 --warmup 3 --no-match --no-cpu-baseline --no-e2e"
-MATCH="--requests 4 --wave 4 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+SMALL="--requests 16 --wave 16 --steps 2 --warmup 3 --no-match --no-cpu-baseline --no-e2e --no-tier"
+MATCH="--requests 4 --wave 4 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-tier"
 TAG=${TAG:-r01}
 
 # 1. launch list of the transfer step (every kernel with its device time)
