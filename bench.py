@@ -430,7 +430,7 @@ def run_kvx(args):
     from paper_2407_00079_b200 import kvx
     from paper_2407_00079_b200.cluster import (exchange_with_peer, max_over_ranks,
                                                pair_topology, sum_over_ranks)
-    from paper_2407_00079_b200.streamer import NcclStreamer, Streamer
+    from paper_2407_00079_b200.streamer import Streamer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -478,13 +478,7 @@ def run_kvx(args):
         dst.tensor_view().zero_()
 
     host_src, host_dst = plan["host_src"], plan["host_dst"]
-    if mode == "peer_nccl":
-        st = NcclStreamer("sender" if role.role == "prefill" else "receiver",
-                          src if src is not None else dst, role.peer, args.ring, slot_bytes)
-        peer = exchange_with_peer(role, {"tables": host_dst})
-        if role.role == "prefill":
-            host_dst = peer["tables"]
-    elif role.role == "local":
+    if role.role == "local":
         st = Streamer(mode, "local", src, dst, args.ring, slot_bytes)
     else:
         st = Streamer(mode, "sender" if role.role == "prefill" else "receiver", src, dst,

@@ -338,8 +338,11 @@ enum {
   KVX_STREAM_LOCAL_STAGED = 1, /* one GPU: gather -> ring -> scatter */
   KVX_STREAM_PEER_FUSED = 2,   /* sender kernel stores into the receiver's pool */
   KVX_STREAM_PEER_CE = 3,      /* gather -> copy engine P2P -> scatter on the receiver */
-  KVX_STREAM_PEER_PULL = 4     /* receiver kernel loads the sender's pool (IPC view) over
+  KVX_STREAM_PEER_PULL = 4,    /* receiver kernel loads the sender's pool (IPC view) over
                                   NVLink and stores locally; the prefill GPU's SMs stay free */
+  KVX_STREAM_PEER_NCCL = 5     /* comparison: gather -> ncclSend / ncclRecv on the pair's own
+                                  2-rank communicator (libnccl.so.2 loaded at run time,
+                                  created in connect: both ends must connect) -> scatter */
 };
 enum { KVX_ROLE_LOCAL = 0, KVX_ROLE_SENDER = 1, KVX_ROLE_RECEIVER = 2 };
 
@@ -399,6 +402,21 @@ int kvx_streamer_check(kvx_streamer* s);
  * match): peer modes then wait only with stream memory operations, never
  * inside a kernel. */
 int kvx_streamer_same_gpu(const kvx_streamer* s);
+/* How a PEER_PULL receiver waits for the sender's units (default GATE, or
+ * $KVX_PULL_GATE at connect; call after connect to override):
+ *   GATE    a one-warp kernel waits, the copy follows it programmatically
+ *           dependent -- near the link peak also for 8 MiB units; only one
+ *           warp is resident while the prefill has not produced the layer
+ *   INLINE  the copy's CTAs wait themselves (the whole next-unit grid stays
+ *           resident while waiting; fastest for tiny units)
+ *   STREAM  the stream front end waits (cuStreamWaitValue64), nothing is
+ *           resident: the choice when the decode GPU runs whole-SM kernels
+ *           (persistent GEMMs) that any co-resident CTA would delay
+ * profiles/r02 and DESIGN.md section 5 have the measured trade-off. */
+#define KVX_PULL_WAIT_GATE 0
+#define KVX_PULL_WAIT_INLINE 1
+#define KVX_PULL_WAIT_STREAM 2
+int kvx_streamer_set_pull_wait(kvx_streamer* s, int mode);
 /* CUDA-graph record / replay of one step (LOCAL_FUSED only): the sends issued
  * between record_begin and record_end are captured, not run; each replay runs
  * them again with one cudaGraphLaunch on the streamer's queue (tables are read

@@ -22,6 +22,10 @@
 //                 the receiver's ring (IPC), the receiver scatters; 64-bit flags
 //                 written with stream memory operations order the three queues
 //                 across processes (no kernel ever spins on another's flag).
+//   PEER_NCCL     comparison: gather -> ncclSend / ncclRecv (a 2-rank NCCL
+//                 communicator of the pair, libnccl loaded at run time) ->
+//                 scatter; sends / receives on a second queue, ring slots
+//                 ordered by events.
 // Sequence numbers only grow, so flags never need resetting (no ABA).
 // The two ends may also be two processes on ONE GPU (same device UUID in the
 // handshake): then no kernel ever waits for the other process -- every wait is
@@ -29,8 +33,11 @@
 // processes sharing a GPU run at the same time.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -58,6 +65,8 @@ struct kvx_streamer {
   uint64_t* pull_status = nullptr;   // PEER_PULL receiver: nonzero once a unit's gate timed out
   bool same_gpu = false;             // the peer process runs on this very GPU
   int pull_wait = 0;                 // PEER_PULL receiver: kPullGate / kPullInline / kPullStream
+  void* nccl_comm = nullptr;         // PEER_NCCL: the pair's 2-rank communicator
+  uint8_t nccl_id[128] = {};         // PEER_NCCL: the sender's ncclUniqueId
   uint64_t* peer_flag = nullptr;     // the peer's flag word, mapped here
   kvx_pool* peer_view = nullptr;     // PEER_FUSED: receiver's pool as seen by the sender
   uint64_t seq = 0;                  // units issued (sender) / consumed (receiver)
@@ -160,7 +169,49 @@ int pull_wait_mode() {
 
 bool is_peer(const kvx_streamer* s) {
   return s->d.mode == KVX_STREAM_PEER_FUSED || s->d.mode == KVX_STREAM_PEER_CE ||
-         s->d.mode == KVX_STREAM_PEER_PULL;
+         s->d.mode == KVX_STREAM_PEER_PULL || s->d.mode == KVX_STREAM_PEER_NCCL;
+}
+
+// ---- NCCL, loaded at run time (PEER_NCCL only): libkvx has no link-time
+// NCCL dependency; in a process that already loaded libnccl.so.2 (e.g. with
+// torch) dlopen returns that same library.
+struct Nccl {
+  int (*get_unique_id)(void*) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  void* init_rank = nullptr;  // ncclCommInitRank(ncclComm_t*, int, ncclUniqueId, int)
+  bool ok = false;
+};
+struct Id128 {  // ncclUniqueId (passed by value to ncclCommInitRank)
+  char b[128];
+};
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    n.get_unique_id = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclGetUniqueId"));
+    n.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+    n.send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(h, "ncclSend"));
+    n.recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(h, "ncclRecv"));
+    n.error_string = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+    n.init_rank = dlsym(h, "ncclCommInitRank");
+    n.ok = n.get_unique_id && n.comm_destroy && n.send && n.recv && n.init_rank;
+  });
+  return n;
+}
+constexpr int kNcclUint8 = 0;  // ncclUint8 in nccl.h's ncclDataType_t
+
+int nccl_error(int rc, const char* where) {
+  const char* msg = nccl().error_string ? nccl().error_string(rc) : "?";
+  return set_error(KVX_ECUDA, std::string(where) + ": NCCL error " + std::to_string(rc) + " (" +
+                                  msg + ")");
 }
 
 struct ExportBlob {
@@ -172,6 +223,7 @@ struct ExportBlob {
   uint8_t flag[KVX_IPC_HANDLE_BYTES];
   uint8_t pool[KVX_IPC_HANDLE_BYTES];
   uint8_t uuid[16];  // the exporting GPU (two processes may share one GPU)
+  uint8_t nccl_id[128];  // PEER_NCCL: the sender's ncclUniqueId
   // followed by ring * KVX_IPC_HANDLE_BYTES slot handles
 };
 constexpr int32_t kMagic = 0x6b767873;  // "kvxs"
@@ -184,14 +236,15 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
                         kvx_streamer** out) {
   KVX_REQUIRE(desc && out, "kvx_streamer_create: NULL argument");
   const int mode = desc->mode, role = desc->role;
-  KVX_REQUIRE(mode >= KVX_STREAM_LOCAL_FUSED && mode <= KVX_STREAM_PEER_PULL,
+  KVX_REQUIRE(mode >= KVX_STREAM_LOCAL_FUSED && mode <= KVX_STREAM_PEER_NCCL,
               "kvx_streamer_create: bad mode");
   const bool local = mode == KVX_STREAM_LOCAL_FUSED || mode == KVX_STREAM_LOCAL_STAGED;
   KVX_REQUIRE(local == (role == KVX_ROLE_LOCAL), "kvx_streamer_create: mode/role mismatch");
   KVX_REQUIRE(role != KVX_ROLE_LOCAL || (src && dst), "local streamer needs src and dst pools");
   KVX_REQUIRE(role != KVX_ROLE_SENDER || src, "sender needs a src pool");
   KVX_REQUIRE(role != KVX_ROLE_RECEIVER || dst, "receiver needs a dst pool");
-  const bool staged = mode == KVX_STREAM_LOCAL_STAGED || mode == KVX_STREAM_PEER_CE;
+  const bool staged = mode == KVX_STREAM_LOCAL_STAGED || mode == KVX_STREAM_PEER_CE ||
+                      mode == KVX_STREAM_PEER_NCCL;
   KVX_REQUIRE(!staged || (desc->ring >= 1 && desc->slot_bytes > 0),
               "staged modes need ring >= 1 and slot_bytes > 0");
   auto* s = new kvx_streamer();
@@ -207,7 +260,7 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
   };
   cudaError_t e = cudaStreamCreateWithFlags(&s->s_main, cudaStreamNonBlocking);
   if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: stream"));
-  if (mode == KVX_STREAM_LOCAL_STAGED) {
+  if (mode == KVX_STREAM_LOCAL_STAGED || mode == KVX_STREAM_PEER_NCCL) {
     e = cudaStreamCreateWithFlags(&s->s_second, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(kvx::cuda_error(e, "kvx_streamer_create: stream"));
   }
@@ -238,6 +291,13 @@ int kvx_streamer_create(const kvx_streamer_desc* desc, kvx_pool* src, kvx_pool* 
     int rc = kvx_xfer_create(s->device, &s->xfer);
     if (rc) return fail(rc);
   }
+  if (mode == KVX_STREAM_PEER_NCCL) {
+    if (!nccl().ok) return fail(set_error(KVX_ECUDA, "kvx_streamer_create: libnccl.so.2 not loadable"));
+    if (role == KVX_ROLE_SENDER) {
+      const int rc = nccl().get_unique_id(s->nccl_id);
+      if (rc) return fail(nccl_error(rc, "ncclGetUniqueId"));
+    }
+  }
   *out = s;
   return KVX_OK;
 }
@@ -254,6 +314,7 @@ int kvx_streamer_destroy(kvx_streamer* s) {
   if (s->graph) cudaGraphDestroy(s->graph);
   if (s->s_main) cudaStreamSynchronize(s->s_main);
   if (s->s_second) cudaStreamSynchronize(s->s_second);
+  if (s->nccl_comm) nccl().comm_destroy(s->nccl_comm);
   if (s->xfer) kvx_xfer_destroy(s->xfer);
   for (void* p : s->peer_ring) kvx_ipc_close(p);
   if (s->peer_flag) kvx_ipc_close(s->peer_flag);
@@ -291,6 +352,7 @@ int kvx_streamer_export(kvx_streamer* s, uint8_t* blob, int64_t cap, int64_t* le
   b.slot_bytes = s->d.slot_bytes;
   int rc = device_uuid(s->device, b.uuid);
   if (rc) return rc;
+  std::memcpy(b.nccl_id, s->nccl_id, sizeof(b.nccl_id));
   rc = kvx_ipc_export(s->flag, b.flag);
   if (rc) return rc;
   if (s->d.role == KVX_ROLE_RECEIVER && s->d.mode == KVX_STREAM_PEER_FUSED) {
@@ -339,6 +401,19 @@ int kvx_streamer_connect(kvx_streamer* s, const uint8_t* blob, int64_t len,
     rc = kvx_pool_create_view(&d, p, &s->peer_view);
     if (rc) return rc;
   }
+  if (s->d.mode == KVX_STREAM_PEER_NCCL) {
+    // the pair's communicator: sender rank 0 (its id), receiver rank 1;
+    // collective -- both ends connect at about the same time
+    KVX_REQUIRE(b.ring == static_cast<int32_t>(s->ring.size()) && b.slot_bytes == s->d.slot_bytes,
+                "kvx_streamer_connect: ring shapes differ");
+    KVX_REQUIRE(!s->same_gpu, "kvx_streamer_connect: NCCL needs the two ends on different GPUs");
+    Id128 id;
+    std::memcpy(id.b, s->d.role == KVX_ROLE_SENDER ? s->nccl_id : b.nccl_id, sizeof(id.b));
+    typedef int (*InitRank)(void**, int, Id128, int);
+    const int rc2 = reinterpret_cast<InitRank>(nccl().init_rank)(
+        &s->nccl_comm, 2, id, s->d.role == KVX_ROLE_SENDER ? 0 : 1);
+    if (rc2) return nccl_error(rc2, "ncclCommInitRank");
+  }
   if (s->d.role == KVX_ROLE_SENDER && s->d.mode == KVX_STREAM_PEER_CE) {
     KVX_REQUIRE(b.ring == static_cast<int32_t>(s->ring.size()) && b.slot_bytes == s->d.slot_bytes,
                 "kvx_streamer_connect: ring shapes differ");
@@ -363,7 +438,8 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
   KVX_REQUIRE(s && s->d.role != KVX_ROLE_RECEIVER, "kvx_streamer_send: not a sender");
   KVX_REQUIRE(n >= 0 && chunk_blocks >= 1 && layers_per_chunk >= 1 && layer_lo <= layer_hi,
               "kvx_streamer_send: bad ranges");
-  const bool needs_dst = s->d.mode != KVX_STREAM_PEER_CE && s->d.mode != KVX_STREAM_PEER_PULL;
+  const bool needs_dst = s->d.mode != KVX_STREAM_PEER_CE && s->d.mode != KVX_STREAM_PEER_PULL &&
+                         s->d.mode != KVX_STREAM_PEER_NCCL;
   KVX_REQUIRE(d_src_table && (!needs_dst || d_dst_table), "kvx_streamer_send: NULL table");
   kvx::DeviceGuard g(s->device);
   const int64_t slab = kvx_pool_slab_bytes(s->src);
@@ -450,6 +526,24 @@ int kvx_streamer_send(kvx_streamer* s, const int32_t* d_src_table, const int32_t
           rc = kvx_transfer_signal(s->xfer, s->peer_flag, c + 1);  // unit c landed
           break;
         }
+        case KVX_STREAM_PEER_NCCL: {
+          KVX_REQUIRE(s->nccl_comm, "kvx_streamer_send: not connected");
+          KVX_REQUIRE(payload <= s->d.slot_bytes, "kvx_streamer_send: unit larger than a slot");
+          const int slot = static_cast<int>(c % R);
+          // the send that last read this slot is done before the gather rewrites it
+          if (c >= static_cast<uint64_t>(R)) KVX_CUDA(cudaStreamWaitEvent(s->s_main, s->slot_ev[slot], 0));
+          rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
+            return kvx_gather(s->src, d_src_table + b0, nb, l0, l1, s->ring[slot], s->s_main);
+          });
+          if (rc) return rc;
+          KVX_CUDA(cudaEventRecord(s->gather_ev[slot], s->s_main));
+          KVX_CUDA(cudaStreamWaitEvent(s->s_second, s->gather_ev[slot], 0));
+          const int nrc = nccl().send(s->ring[slot], static_cast<size_t>(payload), kNcclUint8, 1,
+                                      s->nccl_comm, s->s_second);
+          if (nrc) return nccl_error(nrc, "ncclSend");
+          KVX_CUDA(cudaEventRecord(s->slot_ev[slot], s->s_second));
+          break;
+        }
         default:
           return set_error(KVX_EINVAL, "kvx_streamer_send: bad mode");
       }
@@ -510,6 +604,24 @@ int kvx_streamer_recv(kvx_streamer* s, const int32_t* d_src_table, const int32_t
                                       after_gate);
         });
         if (rc) return rc;
+        continue;
+      }
+      if (s->d.mode == KVX_STREAM_PEER_NCCL) {
+        KVX_REQUIRE(s->nccl_comm, "kvx_streamer_recv: not connected");
+        KVX_REQUIRE(payload <= s->d.slot_bytes, "kvx_streamer_recv: unit larger than a slot");
+        const int slot = static_cast<int>(c % R);
+        // the scatter that last read this slot is done before the next receive lands in it
+        if (c >= static_cast<uint64_t>(R)) KVX_CUDA(cudaStreamWaitEvent(s->s_second, s->slot_ev[slot], 0));
+        const int nrc = nccl().recv(s->ring[slot], static_cast<size_t>(payload), kNcclUint8, 0,
+                                    s->nccl_comm, s->s_second);
+        if (nrc) return nccl_error(nrc, "ncclRecv");
+        KVX_CUDA(cudaEventRecord(s->gather_ev[slot], s->s_second));
+        KVX_CUDA(cudaStreamWaitEvent(s->s_main, s->gather_ev[slot], 0));
+        int rc = timed_launch(s, s->s_main, 2.0 * payload, [&] {
+          return kvx_scatter(s->dst, d_dst_table + b0, nb, l0, l1, s->ring[slot], s->s_main);
+        });
+        if (rc) return rc;
+        KVX_CUDA(cudaEventRecord(s->slot_ev[slot], s->s_main));
         continue;
       }
       const int slot = static_cast<int>(c % R);
@@ -680,5 +792,14 @@ int kvx_streamer_check(kvx_streamer* s) {
 }
 
 int kvx_streamer_same_gpu(const kvx_streamer* s) { return s && s->same_gpu ? 1 : 0; }
+
+int kvx_streamer_set_pull_wait(kvx_streamer* s, int mode) {
+  KVX_REQUIRE(s && mode >= KVX_PULL_WAIT_GATE && mode <= KVX_PULL_WAIT_STREAM,
+              "kvx_streamer_set_pull_wait: bad arguments");
+  KVX_REQUIRE(s->d.mode == KVX_STREAM_PEER_PULL && s->d.role == KVX_ROLE_RECEIVER,
+              "kvx_streamer_set_pull_wait: only PEER_PULL receivers wait for units");
+  s->pull_wait = s->same_gpu ? kPullStream : mode;  // one GPU: never a waiting kernel
+  return KVX_OK;
+}
 
 }  // extern "C"

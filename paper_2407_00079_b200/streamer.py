@@ -1,8 +1,7 @@
 """Layer-wise KVCache streaming prefill -> decode (stages 2 -> 3 -> 4).
 
 The engine is C++ in libkvx (``csrc/kvx_stream.cpp``, ``kvx_streamer_*`` in
-include/kvx.h); this module is its Python face plus one comparison variant
-(NCCL send/recv through torch.distributed) that only Python can drive.
+include/kvx.h); this module is its Python face.
 
 Reference behaviour made real: the prefill -> decode stream of a finished
 prefill (proj/src/sim_engine.cpp:455-470; layer-wise launch/wait),
@@ -11,7 +10,8 @@ per-sender FIFO (proj/src/sim_engine.cpp:409-411).
 
 Modes: ``local_fused`` / ``local_staged`` (N = 1), ``peer_fused`` /
 ``peer_ce`` / ``peer_pull`` (a prefill GPU and a decode GPU, one process each),
-``peer_nccl`` (comparison).
+``peer_nccl`` (comparison: gather -> ncclSend / ncclRecv on the pair's own
+communicator, in C++ too).
 """
 from __future__ import annotations
 
@@ -23,7 +23,8 @@ import torch
 from . import kvx
 from .kvx import _L, _i64, _vp, check
 
-MODES = {"local_fused": 0, "local_staged": 1, "peer_fused": 2, "peer_ce": 3, "peer_pull": 4}
+MODES = {"local_fused": 0, "local_staged": 1, "peer_fused": 2, "peer_ce": 3, "peer_pull": 4,
+         "peer_nccl": 5}
 ROLES = {"local": 0, "sender": 1, "receiver": 2}
 
 
@@ -53,6 +54,8 @@ _sig("kvx_streamer_launch_stats", C.c_int, _vp, C.POINTER(_i64), C.POINTER(C.c_d
 _sig("kvx_streamer_units", C.c_uint64, _vp)
 _sig("kvx_streamer_check", C.c_int, _vp)
 _sig("kvx_streamer_same_gpu", C.c_int, _vp)
+_sig("kvx_streamer_set_pull_wait", C.c_int, _vp, C.c_int)
+PULL_WAIT = {"gate": 0, "inline": 1, "stream": 2}
 _sig("kvx_streamer_record_begin", C.c_int, _vp)
 _sig("kvx_streamer_record_end", C.c_int, _vp)
 _sig("kvx_streamer_replay", C.c_int, _vp)
@@ -138,6 +141,10 @@ class Streamer:
         entries).  Call after finish() before using the decode slots."""
         check(_L.kvx_streamer_check(self.h))
 
+    def set_pull_wait(self, mode: str):
+        """PEER_PULL receiver: 'gate' (default), 'inline' or 'stream' (see kvx.h)."""
+        check(_L.kvx_streamer_set_pull_wait(self.h, PULL_WAIT[mode]))
+
     @property
     def same_gpu(self) -> bool:
         """The connected peer process shares this GPU (waits are stream ops only)."""
@@ -153,74 +160,3 @@ class Streamer:
     def replay(self):
         """Run the recorded step again: one cudaGraphLaunch."""
         check(_L.kvx_streamer_replay(self.h))
-
-
-class NcclStreamer:
-    """Comparison variant: gather -> NCCL isend/irecv (torch.distributed) ->
-    scatter.  Uses SMs for the transfer, unlike the copy-engine path."""
-
-    def __init__(self, role: str, pool: kvx.KVPool, peer_rank: int, ring: int, slot_bytes: int):
-        self.role, self.pool, self.peer = role, pool, peer_rank
-        self.device = pool.device
-        self.stream = torch.cuda.Stream(self.device)
-        self.comm = torch.cuda.Stream(self.device)
-        self.ring = [kvx.DeviceBuffer(slot_bytes, self.device) for _ in range(ring)]
-        self.works = [None] * ring
-        self.ev = [torch.cuda.Event() for _ in range(ring)]
-        self.c = 0
-
-    def _units(self, n, chunk_blocks, layer_lo, layer_hi, lpc):
-        cb = chunk_blocks or max(n, 1)
-        for b0 in range(0, n, cb):
-            for l0 in range(layer_lo, layer_hi, lpc):
-                yield b0, min(cb, n - b0), l0, min(layer_hi, l0 + lpc)
-
-    def send(self, src_table, dst_table, layer_lo, layer_hi, chunk_blocks=0, layers_per_chunk=1):
-        for b0, nb, l0, l1 in self._units(src_table.numel(), chunk_blocks, layer_lo, layer_hi,
-                                          layers_per_chunk):
-            slot = self.c % len(self.ring)
-            payload = (l1 - l0) * 2 * nb * self.pool.slab
-            if self.works[slot] is not None:
-                with torch.cuda.stream(self.stream):
-                    self.works[slot].wait()
-            self.pool.gather(src_table[b0:b0 + nb], l0, l1, self.ring[slot].ptr,
-                             stream=self.stream)
-            self.ev[slot].record(self.stream)
-            self.comm.wait_event(self.ev[slot])
-            with torch.cuda.stream(self.comm):
-                self.works[slot] = torch.distributed.isend(
-                    self.ring[slot].tensor()[:payload], self.peer)
-            self.c += 1
-
-    def recv(self, dst_table, layer_lo, layer_hi, chunk_blocks=0, layers_per_chunk=1,
-             src_table=None):
-        for b0, nb, l0, l1 in self._units(dst_table.numel(), chunk_blocks, layer_lo, layer_hi,
-                                          layers_per_chunk):
-            slot = self.c % len(self.ring)
-            payload = (l1 - l0) * 2 * nb * self.pool.slab
-            with torch.cuda.stream(self.stream):
-                torch.distributed.irecv(self.ring[slot].tensor()[:payload], self.peer).wait()
-            self.pool.scatter(dst_table[b0:b0 + nb], l0, l1, self.ring[slot].ptr,
-                              stream=self.stream)
-            self.c += 1
-
-    def finish(self, stream=None):
-        if stream is not None:
-            for q in (self.stream, self.comm):
-                e = torch.cuda.Event()
-                e.record(q)
-                stream.wait_event(e)
-
-    def after(self, stream):
-        for q in (self.stream, self.comm):
-            q.wait_stream(stream)
-
-    def set_timing(self, on, stride=1):
-        pass
-
-    def check(self):
-        torch.cuda.current_stream(self.device).wait_stream(self.stream)
-        torch.cuda.synchronize(self.device)
-
-    def launch_stats(self, reset=True):
-        return None
