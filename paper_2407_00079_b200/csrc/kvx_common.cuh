@@ -85,6 +85,9 @@ int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* d
                     const uint64_t* d_flag, uint64_t value, const uint64_t* d_status,
                     bool after_gate);
 int pull_done(const uint64_t* d_status, uint64_t* d_peer_flag, uint64_t value, void* stream);
+// Requests of a batch in decreasing block count (kvx_hash.cu).
+int order_by_length(const int64_t* d_key_off, int64_t n_req, int32_t* d_order,
+                    unsigned long long* d_ws, cudaStream_t s);
 
 }  // namespace kvx
 

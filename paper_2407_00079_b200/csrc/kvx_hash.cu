@@ -941,6 +941,18 @@ __global__ void __launch_bounds__(kScanThreads) key_offsets_kernel(
 }  // namespace
 }  // namespace kvx
 
+namespace kvx {
+// Requests in decreasing block count (the hash's counting sort), for kernels
+// that schedule long requests first (the prefix match); ws: one u64 of scratch.
+int order_by_length(const int64_t* d_key_off, int64_t n_req, int32_t* d_order,
+                    unsigned long long* d_ws, cudaStream_t s) {
+  KVX_REQUIRE(n_req <= hw::kOrderMaxReq, "order_by_length: batch too large");
+  hw::order_kernel<<<1, 1024, 0, s>>>(d_key_off, n_req, d_order, d_ws);
+  KVX_LAUNCH_CHECK("order_kernel");
+  return KVX_OK;
+}
+}  // namespace kvx
+
 using namespace kvx;
 
 extern "C" int kvx_key_offsets(const int64_t* d_tok_off, int64_t n_req, int64_t bs,

@@ -365,20 +365,24 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
 // and the task ends after the first wave whose windows all lie past it (all
 // windows before the minimum were fully probed: it IS the first miss).  The
 // extra probes are the speculative windows of the wave that holds the miss.
-template <int G, int C>
-__global__ void __launch_bounds__(G * 32) match_group_kernel(
+template <int G, int C, int MINB = 1>
+__global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
     const __grid_constant__ MatchParams p, const int64_t* __restrict__ keys,
     const int64_t* __restrict__ key_off, int64_t n_req, int64_t* __restrict__ len_out,
-    int64_t* __restrict__ best_len, int32_t* __restrict__ best_id) {
+    int64_t* __restrict__ best_len, int32_t* __restrict__ best_id,
+    const int32_t* __restrict__ order) {
   __shared__ long long first_miss;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int64_t kWin = 32 * C;
   const int64_t tasks = n_req * p.n_inst;
-  for (int64_t t = blockIdx.x; t < tasks; t += gridDim.x) {
-    const int64_t r = tasks <= 0xFFFFFFFFll
-                          ? static_cast<int64_t>(static_cast<uint32_t>(t) / static_cast<uint32_t>(p.n_inst))
-                          : t / p.n_inst;
-    const int i = static_cast<int>(t - r * p.n_inst);
+  for (int64_t tt = blockIdx.x; tt < tasks; tt += gridDim.x) {
+    const int64_t ro = tasks <= 0xFFFFFFFFll
+                           ? static_cast<int64_t>(static_cast<uint32_t>(tt) / static_cast<uint32_t>(p.n_inst))
+                           : tt / p.n_inst;
+    const int i = static_cast<int>(tt - ro * p.n_inst);
+    // longest requests first when an order is given (they set the batch time)
+    const int64_t r = order ? static_cast<int64_t>(__ldg(order + ro)) : ro;
+    const int64_t t = r * p.n_inst + i;
     const int64_t* __restrict__ tk = p.keys[i];
     const uint64_t mask = p.mask[i];
     const int64_t base = key_off[r];
@@ -783,10 +787,26 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
     const int64_t cap = static_cast<int64_t>(sm_count(dev)) * (64 / group);  // 2048 threads / SM
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min(tasks, cap)));
     const int threads = 32 * group;
+    static const bool ordered = [] {
+      const char* e = std::getenv("KVX_MATCH_ORDER");  // longest requests first (measurement)
+      return e && e[0] == '1';
+    }();
+    int32_t* order = nullptr;
+    unsigned long long* ows = nullptr;
+    if (ordered && n_req <= (int64_t{1} << 22)) {
+      KVX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&order), n_req * sizeof(int32_t) + 16, s));
+      ows = reinterpret_cast<unsigned long long*>(order + ((n_req + 1) & ~int64_t{1}));
+      int rc = order_by_length(d_key_off, n_req, order, ows, s);
+      if (rc) return rc;
+    }
 #define KVX_MATCH_G(G, C)                                                                  \
   match_group_kernel<G, C><<<blocks, threads, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out, \
-                                                      d_best_len, d_best_id)
-    switch (group * 10 + chains) {
+                                                      d_best_len, d_best_id, order)
+    static const bool full_occ = [] {
+      const char* e = std::getenv("KVX_MATCH_OCC");  // measurement knob
+      return e && e[0] == '1';
+    }();
+    switch (full_occ && group == 2 && chains == 2 ? 220 : group * 10 + chains) {
       case 21: KVX_MATCH_G(2, 1); break;
       case 41: KVX_MATCH_G(4, 1); break;
       case 42: KVX_MATCH_G(4, 2); break;
@@ -795,10 +815,17 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
       case 82: KVX_MATCH_G(8, 2); break;
       case 84: KVX_MATCH_G(8, 4); break;
       case 24: KVX_MATCH_G(2, 4); break;
+      case 220:  // 2 x 2 at full residency: 32 CTAs of 64 threads per SM (<= 32 registers)
+        match_group_kernel<2, 2, 32><<<static_cast<int>(std::max<int64_t>(
+                                          1, std::min<int64_t>(tasks, sm_count(dev) * 32))),
+                                      threads, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out,
+                                                       d_best_len, d_best_id, order);
+        break;
       default: KVX_MATCH_G(2, 2);
     }
 #undef KVX_MATCH_G
     KVX_LAUNCH_CHECK("match_group_kernel");
+    if (order) KVX_CUDA(cudaFreeAsync(order, s));
   } else {
   const int threads = 256;
   const int64_t want = (tasks + (threads / 32) - 1) / (threads / 32);

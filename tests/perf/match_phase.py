@@ -34,12 +34,15 @@ s.synchronize()
 o = Oracle()
 h = o.make_set(content.cpu().numpy())
 _, want_len, want_id = o.match_prefix_batch([h], [0], keys.cpu().numpy(), key_off.cpu().numpy())
-bl = torch.empty(mw.n_req, dtype=torch.int64, device=d)
-bi = torch.empty(mw.n_req, dtype=torch.int32, device=d)
+NREQ = int(os.environ.get("MP_NREQ", mw.n_req))  # the first NREQ requests only (latency probe)
+want_len, want_id = want_len[:NREQ], want_id[:NREQ]
+bl = torch.empty(NREQ, dtype=torch.int64, device=d)
+bi = torch.empty(NREQ, dtype=torch.int32, device=d)
+ko_q = key_off[: NREQ + 1]
 
 
 def match():
-    pkg.match_prefix_batch([idx], [0], keys, key_off, want_lens=False, stream=s, out=(None, bl, bi))
+    pkg.match_prefix_batch([idx], [0], keys, ko_q, want_lens=False, stream=s, out=(None, bl, bi))
 
 
 def timed(after_hash, reps=20):
@@ -62,10 +65,14 @@ def timed(after_hash, reps=20):
     return tot / reps * 1e3, ok
 
 
-g = os.environ.get("KVX_MATCH_GROUP", "4")
-for pin in (0, 1):
+g = os.environ.get("KVX_MATCH_GROUP", "2")
+tag = (f"group={g} chains={os.environ.get('KVX_MATCH_CHAINS', '2')} "
+       f"order={os.environ.get('KVX_MATCH_ORDER', '0')} occ={os.environ.get('KVX_MATCH_OCC', '0')} "
+       f"nreq={NREQ}")
+pins = (0, 1) if os.environ.get("MP_PIN", "1") == "1" else (0,)
+for pin in pins:
     idx.l2_pin(s, bool(pin))
     for ah in (False, True):
         us, ok = timed(ah)
-        print(f"group={g} pin={pin} after_hash={int(ah)} match {us:.1f} us parity={ok}", flush=True)
+        print(f"{tag} pin={pin} after_hash={int(ah)} match {us:.1f} us parity={ok}", flush=True)
 idx.l2_pin(s, False)
