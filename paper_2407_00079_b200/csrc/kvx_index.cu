@@ -279,6 +279,65 @@ __device__ __forceinline__ void probe_multi(const int64_t* __restrict__ tk, uint
   }
 }
 
+// Sector probing: each round loads the whole 32-byte sector (4 slots) that
+// holds a chain's next slot with one 256-bit load and scans it, so a
+// linear-probe chain resolves in one round unless it runs past its sector
+// (rare at the index's <= 0.40 load) -- against one round per slot when
+// probing slot by slot.  The prefix match is latency bound (a warp step waits
+// for the slowest of its probes), so rounds, not bytes, set its time.
+__device__ __forceinline__ void ld_sector(const int64_t* p, int64_t (&w)[4]) {
+  asm volatile("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3])
+               : "l"(p));
+}
+
+template <int U>
+__device__ __forceinline__ void probe_sector(const int64_t* __restrict__ tk, uint64_t mask,
+                                             const int64_t (&k)[U], const bool (&v)[U],
+                                             bool (&hit)[U]) {
+  bool done[U];
+  uint64_t base[U];
+  int off[U];
+  bool all = true;
+#pragma unroll
+  for (int j = 0; j < U; ++j) {
+    done[j] = !v[j] || is_reserved(k[j]);
+    hit[j] = false;
+    const uint64_t s = mix64(static_cast<uint64_t>(k[j])) & mask;
+    base[j] = s & ~uint64_t{3};  // tables have >= 1024 slots: sectors never wrap
+    off[j] = static_cast<int>(s & 3);
+    all = all && done[j];
+  }
+  while (!all) {
+    int64_t w[U][4];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (!done[j]) ld_sector(tk + base[j], w[j]);
+    }
+    all = true;
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (!done[j]) {
+        bool found = false, empty = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool act = q >= off[j] && !found && !empty;
+          found = found || (act && w[j][q] == k[j]);
+          empty = empty || (act && w[j][q] == kKeyEmpty);
+        }
+        if (found || empty) {
+          hit[j] = found;
+          done[j] = true;
+        } else {
+          base[j] = (base[j] + 4) & mask;
+          off[j] = 0;
+        }
+      }
+      all = all && done[j];
+    }
+  }
+}
+
 #ifndef KVX_PROBE_CHAINS
 #define KVX_PROBE_CHAINS 4
 #endif
@@ -365,7 +424,7 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
 // and the task ends after the first wave whose windows all lie past it (all
 // windows before the minimum were fully probed: it IS the first miss).  The
 // extra probes are the speculative windows of the wave that holds the miss.
-template <int G, int C, int MINB = 1>
+template <int G, int C, int MINB = 1, bool kSector = false>
 __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
     const __grid_constant__ MatchParams p, const int64_t* __restrict__ keys,
     const int64_t* __restrict__ key_off, int64_t n_req, int64_t* __restrict__ len_out,
@@ -401,7 +460,8 @@ __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
           qv[j] = idx < n;
           qk[j] = qv[j] ? __ldg(q + idx) : 0;
         }
-        probe_multi<C>(tk, mask, qk, qv, hit);
+        if (kSector) probe_sector<C>(tk, mask, qk, qv, hit);
+        else probe_multi<C>(tk, mask, qk, qv, hit);
 #pragma unroll
         for (int j = 0; j < C; ++j) {
           const unsigned miss = __ballot_sync(0xffffffffu, !hit[j] && qv[j]);
@@ -802,11 +862,27 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
 #define KVX_MATCH_G(G, C)                                                                  \
   match_group_kernel<G, C><<<blocks, threads, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out, \
                                                       d_best_len, d_best_id, order)
+    static const bool sector = [] {
+      const char* e = std::getenv("KVX_MATCH_SECTOR");  // 0: slot-by-slot probing
+      return !(e && e[0] == '0');
+    }();
     static const bool full_occ = [] {
       const char* e = std::getenv("KVX_MATCH_OCC");  // measurement knob
       return e && e[0] == '1';
     }();
-    switch (full_occ && group == 2 && chains == 2 ? 220 : group * 10 + chains) {
+    switch (sector ? 1000 + group * 10 + chains
+                   : (full_occ && group == 2 && chains == 2 ? 220 : group * 10 + chains)) {
+#define KVX_MATCH_GS(G, C)                                                                    \
+  match_group_kernel<G, C, 1, true><<<blocks, threads, 0, s>>>(p, d_keys, d_key_off, n_req,     \
+                                                               d_len_out, d_best_len, d_best_id, \
+                                                               order)
+      case 1021: KVX_MATCH_GS(2, 1); break;
+      case 1022: KVX_MATCH_GS(2, 2); break;
+      case 1024: KVX_MATCH_GS(2, 4); break;
+      case 1041: KVX_MATCH_GS(4, 1); break;
+      case 1042: KVX_MATCH_GS(4, 2); break;
+      case 1081: KVX_MATCH_GS(8, 1); break;
+#undef KVX_MATCH_GS
       case 21: KVX_MATCH_G(2, 1); break;
       case 41: KVX_MATCH_G(4, 1); break;
       case 42: KVX_MATCH_G(4, 2); break;
