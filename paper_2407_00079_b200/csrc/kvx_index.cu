@@ -449,17 +449,30 @@ __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
     const int64_t* __restrict__ q = keys + base;
     if (threadIdx.x == 0) first_miss = n;  // no miss: the whole chain matches
     __syncthreads();
+    // this warp's query keys of the first wave; each wave then loads the next
+    // wave's keys before probing, so their L2 round trip overlaps the probes
+    int64_t nq[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) {
+      const int64_t idx = warp * kWin + 32 * j + lane;
+      nq[j] = idx < n ? __ldg(q + idx) : 0;
+    }
     for (int64_t wave = 0;; ++wave) {
       const int64_t k0 = (wave * G + warp) * kWin;
-      if (k0 < n && k0 < static_cast<int64_t>(*reinterpret_cast<volatile long long*>(&first_miss))) {
-        int64_t qk[C];
-        bool qv[C], hit[C];
+      int64_t qk[C];
+#pragma unroll
+      for (int j = 0; j < C; ++j) qk[j] = nq[j];
+      if (k0 + G * kWin < n) {
 #pragma unroll
         for (int j = 0; j < C; ++j) {
-          const int64_t idx = k0 + 32 * j + lane;
-          qv[j] = idx < n;
-          qk[j] = qv[j] ? __ldg(q + idx) : 0;
+          const int64_t idx = k0 + G * kWin + 32 * j + lane;
+          nq[j] = idx < n ? __ldg(q + idx) : 0;
         }
+      }
+      if (k0 < n && k0 < static_cast<int64_t>(*reinterpret_cast<volatile long long*>(&first_miss))) {
+        bool qv[C], hit[C];
+#pragma unroll
+        for (int j = 0; j < C; ++j) qv[j] = k0 + 32 * j + lane < n;
         if (kSector) probe_sector<C>(tk, mask, qk, qv, hit);
         else probe_multi<C>(tk, mask, qk, qv, hit);
 #pragma unroll
