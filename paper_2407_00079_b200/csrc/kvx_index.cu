@@ -875,10 +875,16 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
 #define KVX_MATCH_G(G, C)                                                                  \
   match_group_kernel<G, C><<<blocks, threads, 0, s>>>(p, d_keys, d_key_off, n_req, d_len_out, \
                                                       d_best_len, d_best_id, order)
-    static const bool sector = [] {
-      const char* e = std::getenv("KVX_MATCH_SECTOR");  // 0: slot-by-slot probing
-      return !(e && e[0] == '0');
+    // Sector probing shortens each probe chain to ~one dependent round, which
+    // is what a small batch waits for (148 requests: 18.9 vs 24.3 us); a full
+    // Config 4 batch is set by the burst of its first wave through L2, where
+    // the 256-bit loads cost more than they save (34.8 vs 32.7 us):
+    // profiles/r02/match.md.  KVX_MATCH_SECTOR=0/1 forces either.
+    static const int sector_knob = [] {
+      const char* e = std::getenv("KVX_MATCH_SECTOR");
+      return e ? std::atoi(e) : -1;
     }();
+    const bool sector = sector_knob >= 0 ? sector_knob == 1 : tasks <= 1024;
     static const bool full_occ = [] {
       const char* e = std::getenv("KVX_MATCH_OCC");  // measurement knob
       return e && e[0] == '1';
