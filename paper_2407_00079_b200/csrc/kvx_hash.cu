@@ -684,9 +684,45 @@ __device__ __forceinline__ void cp_async16_pred(uint32_t dst, const void* src, i
       "l"(src), "r"(bytes), "l"(pol), "r"(static_cast<int>(on)));
 }
 
-// Branch-free issue of the cursor's sub-round into `slot` (see issue()).
+// Issue of the cursor's sub-round into `slot` (see issue()): the descriptor
+// and the rows of full blocks without branches (five 16-byte copies each);
+// a row that reaches past its request's last token -- the last round of a
+// request only -- takes the zero-filling copies behind one warp-uniform,
+// rarely taken branch, so the common path carries no per-chunk size math.
 __device__ __forceinline__ void issue_p(const Cursor& c, HalfSmem& H, int slot, int hl, int j,
                                         int bs, int nsub, const int32_t* tokens) {
+  const int nb = c.live ? min(kContentLanes, c.nblk - kContentLanes * c.k) : 0;
+  SubDesc d;
+  d.rem0 = c.ntok - kContentLanes * c.k * bs - 16 * c.u;
+  d.nb = nb;
+  d.flags = (c.u == 0 ? 1 : 0) | (c.u == nsub - 1 ? 2 : 0) | (c.k == 0 ? 4 : 0);
+  d.m = c.m;
+  d.kb = c.kb0 + static_cast<int64_t>(kContentLanes) * c.k;
+  d.pad = 0;
+  if (hl == 0) H.desc[slot] = d;  // predicated stores
+  const bool copy = j >= 0 && j < nb;
+  const bool full = c.prem >= 20;
+  const int row = copy ? j : 0;
+  const uint32_t dst =
+      static_cast<uint32_t>(__cvta_generic_to_shared(&H.tok[slot][row * kRowWords]));
+#pragma unroll
+  for (int q = 0; q < 5; ++q) cp_async16_pred(dst + 16 * q, c.a + 4 * q, 16, copy && full);
+  if (__any_sync(0xffffffffu, copy && !full)) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const int bytes = max(0, min(4, c.prem - 4 * q)) * 4;
+      cp_async16_pred(dst + 16 * q, bytes ? static_cast<const void*>(c.a + 4 * q)
+                                          : static_cast<const void*>(tokens),
+                      bytes, copy && !full);
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// The r02 first cut of issue_p (every chunk's size computed every sub-round);
+// kept for the measurement knob KVX_HASH_ISSUE=0.
+__device__ __forceinline__ void issue_p0(const Cursor& c, HalfSmem& H, int slot, int hl, int j,
+                                         int bs, int nsub, const int32_t* tokens) {
   const int nb = c.live ? min(kContentLanes, c.nblk - kContentLanes * c.k) : 0;
   SubDesc d;
   d.rem0 = c.ntok - kContentLanes * c.k * bs - 16 * c.u;
@@ -756,6 +792,7 @@ __device__ __forceinline__ Ctl make_ctl(HalfSmem& H, const uint32_t* zero, int s
   return c;
 }
 
+template <bool kLazyIssue>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
     int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
@@ -787,7 +824,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
   claim(P, true, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
 #pragma unroll 1
   for (int i = 0; i < kPrefetch; ++i) {
-    issue_p(P, H, i, hl, j, bs, nsub, tokens);
+    if (kLazyIssue) issue_p(P, H, i, hl, j, bs, nsub, tokens);
+    else issue_p0(P, H, i, hl, j, bs, nsub, tokens);
     const bool need = step_cursor_p(P, bs, nsub);
     if (__any_sync(0xffffffffu, need))
       claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
@@ -824,10 +862,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
       }
       if (folder) h = fn > 0 ? h14 : h0;
       // next sub-round's work, scheduled into the chain's idle issue slots
-      issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
+      // (the descriptor read first: issue_p ends in its rare branch)
+      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
+      if (kLazyIssue) issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
+      else issue_p0(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
       need = step_cursor_p(P, bs, nsub);
       asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
-      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
     } else {
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
@@ -837,10 +877,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
         h = act ? hn : h;
         if (folder && fn > 0 && act) keys[fkb + s] = h;
       }
-      issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
+      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
+      if (kLazyIssue) issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
+      else issue_p0(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
       need = step_cursor_p(P, bs, nsub);
       asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
-      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
     }
     // hand the finished round's contents to the folder (read next sub-round)
     if (round_done && !folder) {
@@ -1023,7 +1064,10 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
       KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hw::kMaxCtaSmem)));
-      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p,
+      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(hw::kMaxCtaSmem)));
+      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p<false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hw::kMaxCtaSmem)));
       W.hw_attr[dev] = true;
@@ -1063,10 +1107,16 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
       const char* e = std::getenv("KVX_HASH_PIPE");  // 0: the r01 loop (measurement knob)
       return e ? std::atoi(e) : 1;
     }();
+    static const bool lazy_issue = [] {
+      const char* e = std::getenv("KVX_HASH_ISSUE");  // 0: per-chunk sizes every sub-round
+      return !(e && e[0] == '0');
+    }();
     if (pipelined) {
-      KVX_CUDA(cudaLaunchKernelEx(&cfg, hw::halfwarp_hash_kernel_p, d_tokens, d_tok_off, n_req,
-                                  bsi, d_key_off, d_keys, static_cast<const int32_t*>(order), ctr,
-                                  order ? prio : 0));
+      KVX_CUDA(cudaLaunchKernelEx(&cfg,
+                                  lazy_issue ? hw::halfwarp_hash_kernel_p<true>
+                                             : hw::halfwarp_hash_kernel_p<false>,
+                                  d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
+                                  static_cast<const int32_t*>(order), ctr, order ? prio : 0));
     } else {
       KVX_CUDA(cudaLaunchKernelEx(&cfg,
                                   fma_shifts ? hw::halfwarp_hash_kernel<1, true>
