@@ -1164,11 +1164,13 @@ def bench_host_tier(args, dev):
     host.fill_synthetic(7)
     torch.cuda.synchronize()  # the fill runs on the current stream, the loads on io's queue
     rng = np.random.default_rng(12)
-    ht = torch.as_tensor(rng.permutation(host_slots)[: n_pre + n_new].astype(np.int32), device=d)
-    dt = torch.as_tensor(rng.permutation(1024)[: n_pre + n_new].astype(np.int32), device=d)
+    # scattered blocks: DRAM slots drawn from [0, 1024), HBM from [0, 512); contiguous
+    # runs: DRAM [1024, 1280) / [1280, 1536), HBM [512, 768) / [768, 1024) -- disjoint,
+    # so one path's stores never overwrite the other path's source blocks
+    ht = torch.as_tensor(rng.permutation(1024)[: n_pre + n_new].astype(np.int32), device=d)
+    dt = torch.as_tensor(rng.permutation(512)[: n_pre + n_new].astype(np.int32), device=d)
     h_pre, d_pre = ht[:n_pre], dt[:n_pre]
     h_new, d_new = ht[n_pre:], dt[n_pre:]
-    # contiguous runs: DRAM slots [1024, 1280) / [1280, 1536), HBM [512, 768) / [768, 1024)
     ch_pre, cd_pre, ch_new, cd_new = 1024, 512, 1280, 768
     slab = hbm.slab
     load_bytes = L * 2 * n_pre * slab
