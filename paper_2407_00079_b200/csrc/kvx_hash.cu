@@ -862,12 +862,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
       }
       if (folder) h = fn > 0 ? h14 : h0;
       // next sub-round's work, scheduled into the chain's idle issue slots
-      // (the descriptor read first: issue_p ends in its rare branch)
-      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
       if (kLazyIssue) issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
       else issue_p0(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
       need = step_cursor_p(P, bs, nsub);
       asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
+      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
     } else {
 #pragma unroll
       for (int s = 0; s < 16; ++s) {
@@ -877,11 +876,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
         h = act ? hn : h;
         if (folder && fn > 0 && act) keys[fkb + s] = h;
       }
-      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
       if (kLazyIssue) issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
       else issue_p0(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
       need = step_cursor_p(P, bs, nsub);
       asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
+      cn = make_ctl(H, S.zero, nslot, folder, j, bs, fn_next);
     }
     // hand the finished round's contents to the folder (read next sub-round)
     if (round_done && !folder) {
