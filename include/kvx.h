@@ -144,6 +144,19 @@ int kvx_match_prefix_batch(const kvx_index* const* idx, const int32_t* inst_ids,
                            int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
                            void* stream);
 
+/* Stage 1 in one call: kvx_chain_hash_batch, then kvx_match_prefix_batch on
+ * the keys -- with the match of each request starting as soon as the hash
+ * has stored that request's keys (a consumer kernel beside the hash works
+ * through the hash's completion queue), so the batch's match hides under the
+ * hash's long-request tail.  Same arguments and results as the two calls; d_keys
+ * receives the keys.  Block sizes the half-warp hash does not take run the two
+ * calls in sequence. */
+int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req,
+                         int64_t bs, const int64_t* d_key_off, int64_t* d_keys,
+                         const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+                         int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
+                         void* stream);
+
 /* Same query, leaving per request the packed word (len << 32 | ~ordered(id))
  * whose MAXIMUM is the best match with the lowest-id tie-break: instances
  * held by different GPUs combine with one all-reduce(MAX) over these words

@@ -335,11 +335,28 @@ __device__ __forceinline__ int64_t chain_hash_hw(int64_t prev, uint64_t content,
 struct alignas(16) SubDesc {
   int32_t rem0;   // tokens from block 0's position in this sub-round to the request end
   int32_t nb;     // blocks in the round (0: no work)
-  int32_t flags;  // 1: first sub-round of the block, 2: last (round done), 4: round 0 of the request
+  int32_t flags;  // 1: first sub-round of the block, 2: last (round done), 4: round 0 of the
+                  // request, 8: last round of the request
   int32_t m;      // token misalignment of the request (all its blocks share it: bs % 16 == 0)
   int64_t kb;     // key index of block 0 of the round
-  int64_t pad;
+  int64_t r;      // request index
 };
+
+// Completed-request queue (kvx_hash_match_batch): a half-warp that stored
+// the last key of request r appends r; a consumer kernel running beside the
+// hash matches requests in completion order.
+struct Publish {
+  int32_t* queue;            // n_req entries, -1 = not yet written
+  unsigned long long* ctr;   // next queue slot
+};
+
+__device__ __forceinline__ void publish(const Publish& pub, int64_t r) {
+  __threadfence();  // the request's keys before its queue entry
+  const unsigned long long slot = atomicAdd(pub.ctr, 1ull);
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pub.queue + slot),
+               "r"(static_cast<int32_t>(r))
+               : "memory");
+}
 
 // Staging of one request stream (one chain per lane) of one half-warp.
 struct HalfSmem {
@@ -361,6 +378,7 @@ struct Cursor {
   int32_t prem;      // tokens from a to the request end
   int32_t ntok, nblk, k, u, m;
   int64_t kb0;
+  int64_t r;  // request index
   bool live;
 };
 
@@ -374,7 +392,7 @@ __device__ __forceinline__ void claim(Cursor& c, bool need, int hl, int j, int b
                                       const int64_t* __restrict__ key_off, int64_t n_req,
                                       const int32_t* __restrict__ order,
                                       unsigned long long* ctr, unsigned long long& first,
-                                      unsigned long long base) {
+                                      unsigned long long base, const Publish* pub = nullptr) {
   while (__any_sync(0xffffffffu, need)) {
     unsigned long long idx = 0;
     if (need && first != ~0ull) {
@@ -394,6 +412,7 @@ __device__ __forceinline__ void claim(Cursor& c, bool need, int hl, int j, int b
         c.nblk = static_cast<int32_t>(key_off[r + 1] - kb0);
         c.ntok = static_cast<int32_t>(tok_off[r + 1] - tb0);
         c.kb0 = kb0;
+        c.r = r;
         c.m = static_cast<int32_t>(tb0 & 3);
         c.k = 0;
         c.u = 0;
@@ -402,6 +421,7 @@ __device__ __forceinline__ void claim(Cursor& c, bool need, int hl, int j, int b
         c.prem = c.ntok + c.m - jj * bs;
         c.live = true;
         need = c.nblk <= 0;
+        if (need && pub && hl == 0) publish(*pub, r);  // an empty request is done at once
       }
     }
   }
@@ -427,10 +447,11 @@ __device__ __forceinline__ void issue(const Cursor& c, HalfSmem& H, int slot, in
     SubDesc d;
     d.rem0 = c.ntok - kContentLanes * c.k * bs - 16 * c.u;
     d.nb = nb;
-    d.flags = (c.u == 0 ? 1 : 0) | (c.u == nsub - 1 ? 2 : 0) | (c.k == 0 ? 4 : 0);
+    d.flags = (c.u == 0 ? 1 : 0) | (c.u == nsub - 1 ? 2 : 0) | (c.k == 0 ? 4 : 0) |
+              (kContentLanes * (c.k + 1) >= c.nblk ? 8 : 0);
     d.m = c.m;
     d.kb = c.kb0 + static_cast<int64_t>(kContentLanes) * c.k;
-    d.pad = 0;
+    d.r = c.r;
     H.desc[slot] = d;
   }
   if (j >= 0 && j < nb) {
@@ -695,10 +716,11 @@ __device__ __forceinline__ void issue_p(const Cursor& c, HalfSmem& H, int slot, 
   SubDesc d;
   d.rem0 = c.ntok - kContentLanes * c.k * bs - 16 * c.u;
   d.nb = nb;
-  d.flags = (c.u == 0 ? 1 : 0) | (c.u == nsub - 1 ? 2 : 0) | (c.k == 0 ? 4 : 0);
+  d.flags = (c.u == 0 ? 1 : 0) | (c.u == nsub - 1 ? 2 : 0) | (c.k == 0 ? 4 : 0) |
+            (kContentLanes * (c.k + 1) >= c.nblk ? 8 : 0);
   d.m = c.m;
   d.kb = c.kb0 + static_cast<int64_t>(kContentLanes) * c.k;
-  d.pad = 0;
+  d.r = c.r;
   if (hl == 0) H.desc[slot] = d;  // predicated stores
   const bool copy = j >= 0 && j < nb;
   const bool full = c.prem >= 20;
@@ -727,10 +749,11 @@ __device__ __forceinline__ void issue_p0(const Cursor& c, HalfSmem& H, int slot,
   SubDesc d;
   d.rem0 = c.ntok - kContentLanes * c.k * bs - 16 * c.u;
   d.nb = nb;
-  d.flags = (c.u == 0 ? 1 : 0) | (c.u == nsub - 1 ? 2 : 0) | (c.k == 0 ? 4 : 0);
+  d.flags = (c.u == 0 ? 1 : 0) | (c.u == nsub - 1 ? 2 : 0) | (c.k == 0 ? 4 : 0) |
+            (kContentLanes * (c.k + 1) >= c.nblk ? 8 : 0);
   d.m = c.m;
   d.kb = c.kb0 + static_cast<int64_t>(kContentLanes) * c.k;
-  d.pad = 0;
+  d.r = c.r;
   if (hl == 0) H.desc[slot] = d;  // predicated stores
   const bool copy = j >= 0 && j < nb;
   const int row = copy ? j : 0;
@@ -766,7 +789,7 @@ struct Ctl {
   const uint32_t* hi;
   int lim;        // steps that count for this lane (16 on the fast path)
   int nb, flags;  // of the sub-round's descriptor
-  int64_t kb;
+  int64_t kb, r;
   bool fast, idle;
 };
 
@@ -777,6 +800,7 @@ __device__ __forceinline__ Ctl make_ctl(HalfSmem& H, const uint32_t* zero, int s
   c.nb = d.nb;
   c.flags = d.flags;
   c.kb = d.kb;
+  c.r = d.r;
   if (folder) {
     c.lo = H.clo;
     c.hi = H.chi;
@@ -796,7 +820,8 @@ template <bool kLazyIssue>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
     int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
-    const int32_t* __restrict__ order, unsigned long long* ctr, int prio) {
+    const int32_t* __restrict__ order, unsigned long long* ctr, int prio, Publish pubv) {
+  const Publish* pub = pubv.queue ? &pubv : nullptr;
   extern __shared__ __align__(16) unsigned char hw_smem_raw[];
   WarpSmem<1>& S = reinterpret_cast<WarpSmem<1>*>(hw_smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -808,6 +833,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
   HalfSmem& H = S.h[0][half];
   if (lane < 16) S.zero[lane] = 0;
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // a consumer launched programmatically dependent on this kernel (the prefix
+  // match of kvx_hash_match_batch) may become resident now: every CTA of this
+  // grid already is, so the consumer's waits on the queue always progress
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int nwarps = static_cast<int>(blockDim.x >> 5), warp = static_cast<int>(threadIdx.x >> 5);
   const unsigned long long halves = 2ull * nwarps * gridDim.x;
@@ -821,20 +850,22 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
   P.a = tokens;
   P.prem = P.ntok = P.nblk = P.k = P.u = P.m = 0;
   P.kb0 = 0;
-  claim(P, true, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
+  P.r = 0;
+  claim(P, true, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base, pub);
 #pragma unroll 1
   for (int i = 0; i < kPrefetch; ++i) {
     if (kLazyIssue) issue_p(P, H, i, hl, j, bs, nsub, tokens);
     else issue_p0(P, H, i, hl, j, bs, nsub, tokens);
     const bool need = step_cursor_p(P, bs, nsub);
     if (__any_sync(0xffffffffu, need))
-      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
+      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base, pub);
   }
   // sub-round 0's tokens and control
   asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
   __syncwarp();
   int fn = 0, freset = 0;  // folds of the current sub-round (the previous round's blocks)
   int64_t fkb = 0;
+  int64_t fin = -1;        // request whose LAST keys the folder stores in this sub-round
   Ctl c = make_ctl(H, S.zero, 0, folder, j, bs, 0);
   int64_t h = 0;
 #pragma unroll 1
@@ -887,12 +918,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
       H.clo[j] = static_cast<uint32_t>(h);
       H.chi[j] = static_cast<uint32_t>(static_cast<uint64_t>(h) >> 32);
     }
+    // the folder just stored the last keys of request `fin`: it is complete
+    if (pub && folder && fin >= 0) publish(*pub, fin);
+    fin = round_done && (c.flags & 8) ? c.r : -1;
     fn = fn_next;
     fkb = c.kb;
     freset = c.flags & 4;
     __syncwarp();
     if (__any_sync(0xffffffffu, need))
-      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
+      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base, pub);
     c = cn;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1004,9 +1038,28 @@ extern "C" int kvx_key_offsets(const int64_t* d_tok_off, int64_t n_req, int64_t 
   return KVX_OK;
 }
 
+namespace {
+// The block hash; with pub.queue set (half-warp kernel only) every request is
+// appended to the completion queue once its keys are stored.  *published
+// reports whether the launched kernel publishes.
+int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req, int64_t bs,
+                const int64_t* d_key_off, int64_t* d_keys, void* stream, hw::Publish pub,
+                bool* published);
+}  // namespace
+
 extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_tok_off,
                                     int64_t n_req, int64_t bs, const int64_t* d_key_off,
                                     int64_t* d_keys, void* stream) {
+  bool published = false;
+  return hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream,
+                     hw::Publish{nullptr, nullptr}, &published);
+}
+
+namespace {
+int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req, int64_t bs,
+                const int64_t* d_key_off, int64_t* d_keys, void* stream, hw::Publish pub,
+                bool* published) {
+  *published = false;
   KVX_REQUIRE(n_req >= 0, "kvx_chain_hash_batch: n_req must be >= 0");
   KVX_REQUIRE(bs >= 1 && bs <= (1 << 20), "kvx_chain_hash_batch: block size must be >= 1");
   if (n_req == 0) return KVX_OK;
@@ -1115,7 +1168,8 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
                                   lazy_issue ? hw::halfwarp_hash_kernel_p<true>
                                              : hw::halfwarp_hash_kernel_p<false>,
                                   d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
-                                  static_cast<const int32_t*>(order), ctr, order ? prio : 0));
+                                  static_cast<const int32_t*>(order), ctr, order ? prio : 0, pub));
+      *published = pub.queue != nullptr;
     } else {
       KVX_CUDA(cudaLaunchKernelEx(&cfg,
                                   fma_shifts ? hw::halfwarp_hash_kernel<1, true>
@@ -1144,5 +1198,73 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
   KVX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(block_hash_fused_kernel),
                                        dim3(grid), dim3(kHashThreads), args, 0, s));
   KVX_LAUNCH_CHECK("block_hash_fused_kernel");
+  return KVX_OK;
+}
+
+// Completion queue + its two counters (publish, claim) per (device, stream).
+struct QueueScratch {
+  int32_t* queue = nullptr;
+  unsigned long long* ctr = nullptr;
+  int64_t cap = 0;
+};
+std::mutex g_queue_mu;
+std::map<std::pair<int, void*>, QueueScratch> g_queues;
+}  // namespace
+
+// Stage 1 in one stream-ordered call: the block hash, and the prefix match of
+// each request as soon as the hash has stored its keys (a consumer kernel
+// resident beside the hash works through the hash's completion queue), so
+// the match of the batch hides under the hash's long-request tail instead of
+// following it.  Results are those of kvx_chain_hash_batch followed by
+// kvx_match_prefix_batch; block sizes the half-warp kernel does not take run
+// exactly that sequence.
+extern "C" int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_tok_off,
+                                    int64_t n_req, int64_t bs, const int64_t* d_key_off,
+                                    int64_t* d_keys, const kvx_index* const* idx,
+                                    const int32_t* inst_ids, int64_t n_inst, int64_t* d_len_out,
+                                    int64_t* d_best_len, int32_t* d_best_id, void* stream) {
+  KVX_REQUIRE(n_inst >= 1, "find_best_prefix_match: empty prefill pool");
+  KVX_REQUIRE(n_inst <= KVX_MAX_INSTANCES, "kvx_hash_match_batch: too many instances");
+  KVX_REQUIRE(idx != nullptr && inst_ids != nullptr, "kvx_hash_match_batch: NULL instances");
+  KVX_REQUIRE(n_req >= 0, "kvx_hash_match_batch: n_req must be >= 0");
+  KVX_REQUIRE((d_best_len == nullptr) == (d_best_id == nullptr),
+              "kvx_hash_match_batch: best_len and best_id go together");
+  if (n_req == 0) return KVX_OK;
+  KVX_REQUIRE(d_tok_off && d_key_off && d_keys, "kvx_hash_match_batch: NULL array");
+  int dev = 0;
+  KVX_CUDA(cudaGetDevice(&dev));
+  cudaStream_t s = as_stream(stream);
+  QueueScratch* q = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_queue_mu);
+    q = &g_queues[{dev, stream}];
+    if (q->cap < n_req) {
+      if (q->queue) KVX_CUDA(cudaFree(q->queue));  // cudaFree waits for the device
+      q->queue = nullptr;
+      q->cap = 0;
+      const int64_t cap = std::max<int64_t>(n_req, 4096);
+      const int64_t qbytes = (cap * static_cast<int64_t>(sizeof(int32_t)) + 63) & ~int64_t{63};
+      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&q->queue), qbytes + 64));
+      q->ctr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(q->queue) + qbytes);
+      q->cap = cap;
+    }
+  }
+  KVX_CUDA(cudaMemsetAsync(q->queue, 0xFF, n_req * sizeof(int32_t), s));  // -1: not published
+  KVX_CUDA(cudaMemsetAsync(q->ctr, 0, 2 * sizeof(unsigned long long), s));
+  if (d_best_len && n_inst > 1)  // the packed atomicMax words start at 0
+    KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
+  bool published = false;
+  int rc = hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream,
+                       hw::Publish{q->queue, q->ctr}, &published);
+  if (rc) return rc;
+  if (!published)  // the producer / fold kernel (bs % 16 != 0): hash, then match
+    return kvx_match_prefix_batch(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out,
+                                  d_best_len, d_best_id, stream);
+  rc = match_queue_launch(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out, d_best_len,
+                          d_best_id, q->queue, q->ctr + 1, stream);
+  if (rc) return rc;
+  if (d_best_len && n_inst > 1)
+    return kvx_best_unpack(reinterpret_cast<const uint64_t*>(d_best_len), n_req, d_best_len,
+                           d_best_id, stream);
   return KVX_OK;
 }

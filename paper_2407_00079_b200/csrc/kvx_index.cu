@@ -424,6 +424,71 @@ __global__ void __launch_bounds__(256) match_kernel(const __grid_constant__ Matc
 // and the task ends after the first wave whose windows all lie past it (all
 // windows before the minimum were fully probed: it IS the first miss).  The
 // extra probes are the speculative windows of the wave that holds the miss.
+// One (request r, instance i) task of K2 on a CTA of G warps (first_miss:
+// the CTA's shared word).  Ends with the CTA synchronised.
+template <int G, int C, bool kSector>
+__device__ __forceinline__ void match_task(const MatchParams& p, const int64_t* __restrict__ keys,
+                                           const int64_t* __restrict__ key_off, int64_t r, int i,
+                                           int64_t* __restrict__ len_out,
+                                           int64_t* __restrict__ best_len,
+                                           int32_t* __restrict__ best_id, long long& first_miss) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int64_t kWin = 32 * C;
+  const int64_t t = r * p.n_inst + i;
+  const int64_t* __restrict__ tk = p.keys[i];
+  const uint64_t mask = p.mask[i];
+  const int64_t base = key_off[r];
+  const int64_t n = key_off[r + 1] - base;
+  const int64_t* __restrict__ q = keys + base;
+  if (threadIdx.x == 0) first_miss = n;  // no miss: the whole chain matches
+  __syncthreads();
+  // this warp's query keys of the first wave; each wave then loads the next
+  // wave's keys before probing, so their L2 round trip overlaps the probes
+  int64_t nq[C];
+#pragma unroll
+  for (int j = 0; j < C; ++j) {
+    const int64_t idx = warp * kWin + 32 * j + lane;
+    nq[j] = idx < n ? __ldg(q + idx) : 0;
+  }
+  for (int64_t wave = 0;; ++wave) {
+    const int64_t k0 = (wave * G + warp) * kWin;
+    int64_t qk[C];
+#pragma unroll
+    for (int j = 0; j < C; ++j) qk[j] = nq[j];
+    if (k0 + G * kWin < n) {
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const int64_t idx = k0 + G * kWin + 32 * j + lane;
+        nq[j] = idx < n ? __ldg(q + idx) : 0;
+      }
+    }
+    if (k0 < n && k0 < static_cast<int64_t>(*reinterpret_cast<volatile long long*>(&first_miss))) {
+      bool qv[C], hit[C];
+#pragma unroll
+      for (int j = 0; j < C; ++j) qv[j] = k0 + 32 * j + lane < n;
+      if (kSector) probe_sector<C>(tk, mask, qk, qv, hit);
+      else probe_multi<C>(tk, mask, qk, qv, hit);
+#pragma unroll
+      for (int j = 0; j < C; ++j) {
+        const unsigned miss = __ballot_sync(0xffffffffu, !hit[j] && qv[j]);
+        if (miss) {  // the window's first miss (out-of-range lanes are not misses here)
+          if (lane == 0) atomicMin(&first_miss, static_cast<long long>(k0 + 32 * j + __ffs(miss) - 1));
+          break;
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t fm = static_cast<int64_t>(first_miss);
+    const int64_t covered = (wave + 1) * G * kWin;
+    if (fm < covered || covered >= n) break;  // uniform over the CTA
+  }
+  if (threadIdx.x == 0) {
+    const int64_t len = static_cast<int64_t>(first_miss);
+    match_result(p, t, r, i, len, len_out, best_len, best_id);
+  }
+  __syncthreads();  // first_miss is re-initialised for the next task
+}
+
 template <int G, int C, int MINB = 1, bool kSector = false>
 __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
     const __grid_constant__ MatchParams p, const int64_t* __restrict__ keys,
@@ -431,8 +496,6 @@ __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
     int64_t* __restrict__ best_len, int32_t* __restrict__ best_id,
     const int32_t* __restrict__ order) {
   __shared__ long long first_miss;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int64_t kWin = 32 * C;
   const int64_t tasks = n_req * p.n_inst;
   for (int64_t tt = blockIdx.x; tt < tasks; tt += gridDim.x) {
     const int64_t ro = tasks <= 0xFFFFFFFFll
@@ -441,59 +504,48 @@ __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
     const int i = static_cast<int>(tt - ro * p.n_inst);
     // longest requests first when an order is given (they set the batch time)
     const int64_t r = order ? static_cast<int64_t>(__ldg(order + ro)) : ro;
-    const int64_t t = r * p.n_inst + i;
-    const int64_t* __restrict__ tk = p.keys[i];
-    const uint64_t mask = p.mask[i];
-    const int64_t base = key_off[r];
-    const int64_t n = key_off[r + 1] - base;
-    const int64_t* __restrict__ q = keys + base;
-    if (threadIdx.x == 0) first_miss = n;  // no miss: the whole chain matches
-    __syncthreads();
-    // this warp's query keys of the first wave; each wave then loads the next
-    // wave's keys before probing, so their L2 round trip overlaps the probes
-    int64_t nq[C];
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const int64_t idx = warp * kWin + 32 * j + lane;
-      nq[j] = idx < n ? __ldg(q + idx) : 0;
-    }
-    for (int64_t wave = 0;; ++wave) {
-      const int64_t k0 = (wave * G + warp) * kWin;
-      int64_t qk[C];
-#pragma unroll
-      for (int j = 0; j < C; ++j) qk[j] = nq[j];
-      if (k0 + G * kWin < n) {
-#pragma unroll
-        for (int j = 0; j < C; ++j) {
-          const int64_t idx = k0 + G * kWin + 32 * j + lane;
-          nq[j] = idx < n ? __ldg(q + idx) : 0;
-        }
-      }
-      if (k0 < n && k0 < static_cast<int64_t>(*reinterpret_cast<volatile long long*>(&first_miss))) {
-        bool qv[C], hit[C];
-#pragma unroll
-        for (int j = 0; j < C; ++j) qv[j] = k0 + 32 * j + lane < n;
-        if (kSector) probe_sector<C>(tk, mask, qk, qv, hit);
-        else probe_multi<C>(tk, mask, qk, qv, hit);
-#pragma unroll
-        for (int j = 0; j < C; ++j) {
-          const unsigned miss = __ballot_sync(0xffffffffu, !hit[j] && qv[j]);
-          if (miss) {  // the window's first miss (out-of-range lanes are not misses here)
-            if (lane == 0) atomicMin(&first_miss, static_cast<long long>(k0 + 32 * j + __ffs(miss) - 1));
+    match_task<G, C, kSector>(p, keys, key_off, r, i, len_out, best_len, best_id, first_miss);
+  }
+}
+
+// K2 fed by the block hash running beside it (kvx_hash_match_batch): the
+// hash appends each request to `queue` once its keys are stored; CTAs claim
+// queue slots in order and wait (one thread, acquire loads, back-off) for the
+// slot's request, then match it against every instance.  Launched
+// programmatically dependent on the hash, which triggers only once all of its
+// CTAs are resident, so every awaited slot is eventually written.
+template <int G, int C, bool kSector>
+__global__ void __launch_bounds__(G * 32) match_queue_kernel(
+    const __grid_constant__ MatchParams p, const int64_t* __restrict__ keys,
+    const int64_t* __restrict__ key_off, int64_t n_req, int64_t* __restrict__ len_out,
+    int64_t* __restrict__ best_len, int32_t* __restrict__ best_id, const int32_t* queue,
+    unsigned long long* claim) {
+  __shared__ long long first_miss;
+  __shared__ long long req;
+  while (true) {
+    if (threadIdx.x == 0) {
+      const unsigned long long slot = atomicAdd(claim, 1ull);
+      long long r = -1;
+      if (slot < static_cast<unsigned long long>(n_req)) {
+        unsigned ns = 64;
+        while (true) {
+          int v;
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(queue + slot) : "memory");
+          if (v >= 0) {
+            r = v;
             break;
           }
+          __nanosleep(ns);
+          ns = ns < 2048 ? 2 * ns : ns;
         }
       }
-      __syncthreads();
-      const int64_t fm = static_cast<int64_t>(first_miss);
-      const int64_t covered = (wave + 1) * G * kWin;
-      if (fm < covered || covered >= n) break;  // uniform over the CTA
+      req = r;
     }
-    if (threadIdx.x == 0) {
-      const int64_t len = static_cast<int64_t>(first_miss);
-      match_result(p, t, r, i, len, len_out, best_len, best_id);
-    }
-    __syncthreads();  // first_miss is re-initialised for the next task
+    __syncthreads();
+    const int64_t r = static_cast<int64_t>(req);
+    if (r < 0) return;
+    for (int i = 0; i < p.n_inst; ++i)
+      match_task<G, C, kSector>(p, keys, key_off, r, i, len_out, best_len, best_id, first_miss);
   }
 }
 
@@ -938,6 +990,47 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
   return KVX_OK;
 }
 }  // namespace
+
+namespace kvx {
+// K2 consumer of the hash's completion queue (kvx_hash_match_batch): params
+// as kvx_match_prefix_batch; launched programmatically dependent on the hash.
+int match_queue_launch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+                       const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+                       int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
+                       const int32_t* d_queue, unsigned long long* d_claim, void* stream) {
+  MatchParams p{};
+  p.n_inst = static_cast<int32_t>(n_inst);
+  const int dev = idx[0]->device;
+  for (int64_t i = 0; i < n_inst; ++i) {
+    KVX_REQUIRE(idx[i] != nullptr && idx[i]->device == dev,
+                "kvx_hash_match_batch: NULL index or indices on different devices");
+    p.keys[i] = idx[i]->keys;
+    p.mask[i] = static_cast<uint64_t>(idx[i]->slots - 1);
+    p.ids[i] = inst_ids[i];
+  }
+  DeviceGuard g(dev);
+  // resident beside the hash (one 384-thread CTA per SM): a few 64-thread CTAs per SM
+  const int blocks = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(n_req, static_cast<int64_t>(sm_count(dev)) * 6)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(64);
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (n_req * n_inst <= 1024)
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, match_queue_kernel<2, 2, true>, p, d_keys, d_key_off, n_req,
+                                d_len_out, d_best_len, d_best_id, d_queue, d_claim));
+  else
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, match_queue_kernel<2, 2, false>, p, d_keys, d_key_off, n_req,
+                                d_len_out, d_best_len, d_best_id, d_queue, d_claim));
+  KVX_LAUNCH_CHECK("match_queue_kernel");
+  return KVX_OK;
+}
+}  // namespace kvx
 
 // ---- cross-GPU best match without a collective --------------------------
 // SURVEY 8(e) case ii: one prefill instance (or several) per GPU.  The match

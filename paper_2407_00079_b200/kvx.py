@@ -90,6 +90,8 @@ _sig("kvx_sync", C.c_int, _vp)
 _sig("kvx_chain_hash", _i64, _i64, C.c_uint64)
 _sig("kvx_chain_hash_batch", C.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp)
 _sig("kvx_key_offsets", C.c_int, _vp, _i64, _i64, _vp, _vp)
+_sig("kvx_hash_match_batch", C.c_int, _vp, _vp, _i64, _i64, _vp, _vp, C.POINTER(_vp),
+     C.POINTER(_i32), _i64, _vp, _vp, _vp, _vp)
 _sig("kvx_xmatch_key_buffer", C.c_int, _vp, _i64, C.POINTER(_vp))
 _sig("kvx_xmatch_share_keys", C.c_int, _vp, _i64, _i64, _vp)
 _sig("kvx_index_create", C.c_int, C.c_int, _i64, C.POINTER(_vp))
@@ -342,6 +344,39 @@ def match_prefix_batch(indices: Sequence[BlockIndex], inst_ids: Sequence[int], k
                                     _ptr(key_off), n_req, _ptr(lens) if lens is not None else None,
                                     _ptr(best_len), _ptr(best_id), _stream(stream)))
     return lens, best_len, best_id
+
+
+def hash_match_batch(tokens: torch.Tensor, tok_off: torch.Tensor, bs: int,
+                     indices: Sequence["BlockIndex"], inst_ids: Sequence[int],
+                     key_off: Optional[torch.Tensor] = None, keys: Optional[torch.Tensor] = None,
+                     want_lens: bool = False, stream=None, out=None):
+    """Stage 1 in one call (kvx_hash_match_batch): block keys of the batch and
+    every request's match against the instances, the match of a request
+    starting as soon as its keys are stored.  Returns (keys, key_off, lens or
+    None, best_len, best_id)."""
+    assert tokens.dtype == torch.int32 and tok_off.dtype == torch.int64
+    n_inst = len(indices)
+    n_req = len(tok_off) - 1
+    dev = tokens.device
+    with torch.cuda.stream(_torch_stream(stream, dev)):
+        if key_off is None:
+            key_off = key_offsets(tok_off, bs, stream=stream)
+        if keys is None:
+            n_keys = int(key_off[-1].item())
+            keys = torch.empty(max(n_keys, 1), dtype=torch.int64, device=dev)[:n_keys]
+        if out is None:
+            lens = torch.empty((n_req, n_inst), dtype=torch.int64, device=dev) if want_lens else None
+            best_len = torch.empty(n_req, dtype=torch.int64, device=dev)
+            best_id = torch.empty(n_req, dtype=torch.int32, device=dev)
+        else:
+            lens, best_len, best_id = out
+    arr = (_vp * max(n_inst, 1))(*[i.h for i in indices])
+    ids = (_i32 * max(n_inst, 1))(*[int(i) for i in inst_ids])
+    check(_L.kvx_hash_match_batch(_ptr(tokens) if tokens.numel() else None, _ptr(tok_off),
+                                  n_req, bs, _ptr(key_off), _ptr(keys) if keys.numel() else None,
+                                  arr, ids, n_inst, _ptr(lens) if lens is not None else None,
+                                  _ptr(best_len), _ptr(best_id), _stream(stream)))
+    return keys, key_off, lens, best_len, best_id
 
 
 def match_prefix_packed(indices: Sequence[BlockIndex], inst_ids: Sequence[int],

@@ -298,3 +298,42 @@ def test_config4_scale_match_vs_oracle(kvx, oracle_lib):
     assert np.array_equal(lens.cpu().numpy(), wl)
     assert np.array_equal(bl.cpu().numpy(), wbl)
     assert np.array_equal(bi.cpu().numpy(), wbi)
+
+
+@pytest.mark.parametrize("bs,n_inst,n_req", [(16, 1, 300), (16, 3, 300), (32, 2, 97), (5, 2, 60),
+                                             (16, 1, 40000)])
+def test_hash_match_fused_equals_two_calls(kvx, oracle_lib, bs, n_inst, n_req):
+    """kvx_hash_match_batch (the match of each request started by the hash's
+    completion queue) == kvx_chain_hash_batch + kvx_match_prefix_batch, and
+    == the oracle; ragged, empty and sub-block requests included; bs=5 runs
+    the sequential fallback."""
+    rng = np.random.default_rng(bs * 100 + n_inst)
+    hi = 30 * bs if n_req < 1000 else 60
+    lens = rng.integers(0, hi, size=n_req)
+    lens[:3] = [0, 1, bs]
+    tok_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    tokens = rng.integers(0, 32000, size=int(tok_off[-1]) + 8).astype(np.int32)
+    want_keys, wko = oracle_lib.block_hash_batch(tokens, tok_off, bs)
+    contents = []
+    for i in range(n_inst):  # each instance holds random prefixes of some requests' chains
+        pick = rng.choice(n_req, size=min(n_req, 50), replace=False)
+        ks = [want_keys[wko[p]: wko[p] + int(rng.integers(0, wko[p + 1] - wko[p] + 1))] for p in pick]
+        ks.append(rng.integers(0, 1 << 62, size=20, dtype=np.int64))
+        contents.append(np.concatenate(ks).astype(np.int64))
+    ids = [5 - 2 * i for i in range(n_inst)]
+    idx = [_index(kvx, c) for c in contents]
+    keys, ko, lens_out, bl, bi = kvx.kvx.hash_match_batch(
+        _t(tokens, torch.int32), _t(tok_off, torch.int64), bs, idx, ids, want_lens=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(keys.cpu().numpy(), want_keys)
+    sets = [oracle_lib.make_set(c) for c in contents]
+    wl, wbl, wbi = oracle_lib.match_prefix_batch(sets, ids, want_keys, wko)
+    assert np.array_equal(lens_out.cpu().numpy(), wl)
+    assert np.array_equal(bl.cpu().numpy(), wbl)
+    assert np.array_equal(bi.cpu().numpy(), wbi)
+    # repeated calls on the same stream reuse the completion queue
+    keys2, _, _, bl2, bi2 = kvx.kvx.hash_match_batch(
+        _t(tokens, torch.int32), _t(tok_off, torch.int64), bs, idx, ids)
+    torch.cuda.synchronize()
+    assert np.array_equal(keys2.cpu().numpy(), want_keys)
+    assert np.array_equal(bl2.cpu().numpy(), wbl) and np.array_equal(bi2.cpu().numpy(), wbi)
