@@ -930,6 +930,7 @@ def bench_match(args, dev, rank, world, role):
     ms = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
     total_blocks = sum_over_ranks(float(n_blocks), d)  # every rank's own batch
     value = total_blocks / (ms / 1e3)
+    pkg.kvx.hash_match_check(s)
     if not (np.array_equal(keys.cpu().numpy(), k_ref) and
             np.array_equal(best_len.cpu().numpy(), want_len) and
             np.array_equal(best_id.cpu().numpy(), want_id)):

@@ -156,6 +156,10 @@ int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_tok_off, int6
                          const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
                          int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
                          void* stream);
+/* Host-blocking: KVX_ECUDA if a match task of kvx_hash_match_batch on the
+ * device of `stream` gave up (5 s) waiting for a request the hash never
+ * completed (a defect; its results are then missing), else KVX_OK. */
+int kvx_hash_match_check(void* stream);
 
 /* Same query, leaving per request the packed word (len << 32 | ~ordered(id))
  * whose MAXIMUM is the best match with the lowest-id tie-break: instances

@@ -508,6 +508,9 @@ __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
   }
 }
 
+// Set when a queue consumer gave up waiting for a request (kvx_hash_match_check).
+__device__ unsigned long long g_queue_timeouts = 0;
+
 // K2 fed by the block hash running beside it (kvx_hash_match_batch): the
 // hash appends each request to `queue` once its keys are stored; CTAs claim
 // queue slots in order and wait (one thread, acquire loads, back-off) for the
@@ -528,6 +531,8 @@ __global__ void __launch_bounds__(G * 32) match_queue_kernel(
       long long r = -1;
       if (slot < static_cast<unsigned long long>(n_req)) {
         unsigned ns = 64;
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
         while (true) {
           int v;
           asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(queue + slot) : "memory");
@@ -537,6 +542,11 @@ __global__ void __launch_bounds__(G * 32) match_queue_kernel(
           }
           __nanosleep(ns);
           ns = ns < 2048 ? 2 * ns : ns;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          if (t - t0 > 5000000000ull) {  // 5 s: a request never published -- report, don't hang
+            g_queue_timeouts = 1;
+            break;
+          }
         }
       }
       req = r;
@@ -1031,6 +1041,23 @@ int match_queue_launch(const kvx_index* const* idx, const int32_t* inst_ids, int
   return KVX_OK;
 }
 }  // namespace kvx
+
+extern "C" int kvx_hash_match_check(void* stream) {
+  int dev = -1;
+  if (stream) {
+    KVX_CUDA(cudaStreamGetDevice(as_stream(stream), &dev));
+  } else {
+    KVX_CUDA(cudaGetDevice(&dev));
+  }
+  DeviceGuard g(dev);
+  KVX_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  unsigned long long t = 0, zero = 0;
+  KVX_CUDA(cudaMemcpyFromSymbol(&t, g_queue_timeouts, sizeof(t)));
+  if (!t) return KVX_OK;
+  KVX_CUDA(cudaMemcpyToSymbol(g_queue_timeouts, &zero, sizeof(zero)));
+  return set_error(KVX_ECUDA, "kvx_hash_match_check: a match task waited 5 s for a request the "
+                              "hash never completed; its results are missing");
+}
 
 // ---- cross-GPU best match without a collective --------------------------
 // SURVEY 8(e) case ii: one prefill instance (or several) per GPU.  The match

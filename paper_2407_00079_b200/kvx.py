@@ -92,6 +92,7 @@ _sig("kvx_chain_hash_batch", C.c_int, _vp, _vp, _i64, _i64, _vp, _vp, _vp)
 _sig("kvx_key_offsets", C.c_int, _vp, _i64, _i64, _vp, _vp)
 _sig("kvx_hash_match_batch", C.c_int, _vp, _vp, _i64, _i64, _vp, _vp, C.POINTER(_vp),
      C.POINTER(_i32), _i64, _vp, _vp, _vp, _vp)
+_sig("kvx_hash_match_check", C.c_int, _vp)
 _sig("kvx_xmatch_key_buffer", C.c_int, _vp, _i64, C.POINTER(_vp))
 _sig("kvx_xmatch_share_keys", C.c_int, _vp, _i64, _i64, _vp)
 _sig("kvx_index_create", C.c_int, C.c_int, _i64, C.POINTER(_vp))
@@ -377,6 +378,11 @@ def hash_match_batch(tokens: torch.Tensor, tok_off: torch.Tensor, bs: int,
                                   arr, ids, n_inst, _ptr(lens) if lens is not None else None,
                                   _ptr(best_len), _ptr(best_id), _stream(stream)))
     return keys, key_off, lens, best_len, best_id
+
+
+def hash_match_check(stream=None) -> None:
+    """Host-blocking: raise if a fused stage-1 call lost a request (a defect)."""
+    check(_L.kvx_hash_match_check(_stream(stream)))
 
 
 def match_prefix_packed(indices: Sequence[BlockIndex], inst_ids: Sequence[int],
