@@ -342,19 +342,17 @@ struct alignas(16) SubDesc {
   int64_t r;      // request index
 };
 
-// Completed-request queue (kvx_hash_match_batch): a half-warp that stored
-// the last key of request r appends r; a consumer kernel running beside the
-// hash matches requests in completion order.
+// Key progress per request (kvx_hash_match_batch): after the folding lane
+// stored a round's keys it publishes, with release semantics, the absolute key
+// index up to which request r's keys exist; a match kernel running beside the
+// hash follows each request's progress window by window.
 struct Publish {
-  int32_t* queue;            // n_req entries, -1 = not yet written
-  unsigned long long* ctr;   // next queue slot
+  int64_t* progress;  // n_req entries, 0 before the first round of r
 };
 
-__device__ __forceinline__ void publish(const Publish& pub, int64_t r) {
-  __threadfence();  // the request's keys before its queue entry
-  const unsigned long long slot = atomicAdd(pub.ctr, 1ull);
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pub.queue + slot),
-               "r"(static_cast<int32_t>(r))
+__device__ __forceinline__ void publish(const Publish& pub, int64_t r, int64_t key_end) {
+  __threadfence();  // the keys before the progress word
+  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(pub.progress + r), "l"(key_end)
                : "memory");
 }
 
@@ -421,7 +419,6 @@ __device__ __forceinline__ void claim(Cursor& c, bool need, int hl, int j, int b
         c.prem = c.ntok + c.m - jj * bs;
         c.live = true;
         need = c.nblk <= 0;
-        if (need && pub && hl == 0) publish(*pub, r);  // an empty request is done at once
       }
     }
   }
@@ -821,7 +818,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
     int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
     const int32_t* __restrict__ order, unsigned long long* ctr, int prio, Publish pubv) {
-  const Publish* pub = pubv.queue ? &pubv : nullptr;
+  const Publish* pub = pubv.progress ? &pubv : nullptr;
   extern __shared__ __align__(16) unsigned char hw_smem_raw[];
   WarpSmem<1>& S = reinterpret_cast<WarpSmem<1>*>(hw_smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -865,7 +862,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
   __syncwarp();
   int fn = 0, freset = 0;  // folds of the current sub-round (the previous round's blocks)
   int64_t fkb = 0;
-  int64_t fin = -1;        // request whose LAST keys the folder stores in this sub-round
+  int64_t fold_r = -1;     // request whose round the folder folds in this sub-round
+  int64_t fold_end = 0;    // ... and the absolute key index that round ends at
   Ctl c = make_ctl(H, S.zero, 0, folder, j, bs, 0);
   int64_t h = 0;
 #pragma unroll 1
@@ -918,9 +916,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
       H.clo[j] = static_cast<uint32_t>(h);
       H.chi[j] = static_cast<uint32_t>(static_cast<uint64_t>(h) >> 32);
     }
-    // the folder just stored the last keys of request `fin`: it is complete
-    if (pub && folder && fin >= 0) publish(*pub, fin);
-    fin = round_done && (c.flags & 8) ? c.r : -1;
+    // the folder just stored the keys of a round of request fold_r
+    if (pub && folder && fold_r >= 0) publish(*pub, fold_r, fold_end);
+    fold_r = round_done ? c.r : -1;
+    fold_end = c.kb + c.nb;
     fn = fn_next;
     fkb = c.kb;
     freset = c.flags & 4;
@@ -1044,7 +1043,7 @@ namespace {
 // reports whether the launched kernel publishes.
 int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req, int64_t bs,
                 const int64_t* d_key_off, int64_t* d_keys, void* stream, hw::Publish pub,
-                bool* published);
+                bool* published, const int32_t** order_used = nullptr);
 }  // namespace
 
 extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_tok_off,
@@ -1052,14 +1051,15 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
                                     int64_t* d_keys, void* stream) {
   bool published = false;
   return hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream,
-                     hw::Publish{nullptr, nullptr}, &published);
+                     hw::Publish{nullptr}, &published);
 }
 
 namespace {
 int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req, int64_t bs,
                 const int64_t* d_key_off, int64_t* d_keys, void* stream, hw::Publish pub,
-                bool* published) {
+                bool* published, const int32_t** order_used) {
   *published = false;
+  if (order_used) *order_used = nullptr;
   KVX_REQUIRE(n_req >= 0, "kvx_chain_hash_batch: n_req must be >= 0");
   KVX_REQUIRE(bs >= 1 && bs <= (1 << 20), "kvx_chain_hash_batch: block size must be >= 1");
   if (n_req == 0) return KVX_OK;
@@ -1169,7 +1169,8 @@ int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req
                                              : hw::halfwarp_hash_kernel_p<false>,
                                   d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
                                   static_cast<const int32_t*>(order), ctr, order ? prio : 0, pub));
-      *published = pub.queue != nullptr;
+      *published = pub.progress != nullptr;
+      if (order_used) *order_used = order;
     } else {
       KVX_CUDA(cudaLaunchKernelEx(&cfg,
                                   fma_shifts ? hw::halfwarp_hash_kernel<1, true>
@@ -1201,9 +1202,9 @@ int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req
   return KVX_OK;
 }
 
-// Completion queue + its two counters (publish, claim) per (device, stream).
+// Progress words + the consumer's claim counter per (device, stream).
 struct QueueScratch {
-  int32_t* queue = nullptr;
+  int64_t* progress = nullptr;
   unsigned long long* ctr = nullptr;
   int64_t cap = 0;
 };
@@ -1212,10 +1213,12 @@ std::map<std::pair<int, void*>, QueueScratch> g_queues;
 }  // namespace
 
 // Stage 1 in one stream-ordered call: the block hash, and the prefix match of
-// each request as soon as the hash has stored its keys (a consumer kernel
-// resident beside the hash works through the hash's completion queue), so
-// the match of the batch hides under the hash's long-request tail instead of
-// following it.  Results are those of kvx_chain_hash_batch followed by
+// each request following the hash's key production window by window (a
+// match kernel resident beside the hash takes the requests in the hash's
+// longest-first order and waits per window for the request's published key
+// progress).  A prefix match ends at the first miss, typically long before
+// the request's last key exists, so the match of the batch hides under the
+// hash instead of following it.  Results are those of kvx_chain_hash_batch followed by
 // kvx_match_prefix_batch; block sizes the half-warp kernel does not take run
 // exactly that sequence.
 extern "C" int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_tok_off,
@@ -1239,29 +1242,30 @@ extern "C" int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_to
     std::lock_guard<std::mutex> lk(g_queue_mu);
     q = &g_queues[{dev, stream}];
     if (q->cap < n_req) {
-      if (q->queue) KVX_CUDA(cudaFree(q->queue));  // cudaFree waits for the device
-      q->queue = nullptr;
+      if (q->progress) KVX_CUDA(cudaFree(q->progress));  // cudaFree waits for the device
+      q->progress = nullptr;
       q->cap = 0;
       const int64_t cap = std::max<int64_t>(n_req, 4096);
-      const int64_t qbytes = (cap * static_cast<int64_t>(sizeof(int32_t)) + 63) & ~int64_t{63};
-      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&q->queue), qbytes + 64));
-      q->ctr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(q->queue) + qbytes);
+      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&q->progress), (cap + 8) * sizeof(int64_t)));
+      q->ctr = reinterpret_cast<unsigned long long*>(q->progress + cap);
       q->cap = cap;
     }
   }
-  KVX_CUDA(cudaMemsetAsync(q->queue, 0xFF, n_req * sizeof(int32_t), s));  // -1: not published
-  KVX_CUDA(cudaMemsetAsync(q->ctr, 0, 2 * sizeof(unsigned long long), s));
+  // progress 0 = no key yet; the claim counter 0
+  KVX_CUDA(cudaMemsetAsync(q->progress, 0, n_req * sizeof(int64_t), s));
+  KVX_CUDA(cudaMemsetAsync(q->ctr, 0, sizeof(unsigned long long), s));
   if (d_best_len && n_inst > 1)  // the packed atomicMax words start at 0
     KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
   bool published = false;
+  const int32_t* order = nullptr;
   int rc = hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream,
-                       hw::Publish{q->queue, q->ctr}, &published);
+                       hw::Publish{q->progress}, &published, &order);
   if (rc) return rc;
   if (!published)  // the producer / fold kernel (bs % 16 != 0): hash, then match
     return kvx_match_prefix_batch(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out,
                                   d_best_len, d_best_id, stream);
-  rc = match_queue_launch(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out, d_best_len,
-                          d_best_id, q->queue, q->ctr + 1, stream);
+  rc = match_follow_launch(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out,
+                           d_best_len, d_best_id, q->progress, order, q->ctr, stream);
   if (rc) return rc;
   if (d_best_len && n_inst > 1)
     return kvx_best_unpack(reinterpret_cast<const uint64_t*>(d_best_len), n_req, d_best_len,

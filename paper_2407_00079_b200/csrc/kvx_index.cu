@@ -508,54 +508,106 @@ __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
   }
 }
 
-// Set when a queue consumer gave up waiting for a request (kvx_hash_match_check).
+// Set when a follower gave up waiting for a request's keys (kvx_hash_match_check).
 __device__ unsigned long long g_queue_timeouts = 0;
 
-// K2 fed by the block hash running beside it (kvx_hash_match_batch): the
-// hash appends each request to `queue` once its keys are stored; CTAs claim
-// queue slots in order and wait (one thread, acquire loads, back-off) for the
-// slot's request, then match it against every instance.  Launched
+// K2 following the block hash running beside it (kvx_hash_match_batch).  A
+// CTA takes requests in the hash's own longest-first claim order and, before
+// each wave, waits (thread 0: acquire loads of the request's published key
+// progress, back-off, 5 s limit) until the wave's keys exist.  The match stops
+// at the first miss, usually long before the request's hash ends.  Launched
 // programmatically dependent on the hash, which triggers only once all of its
-// CTAs are resident, so every awaited slot is eventually written.
+// CTAs are resident, so every awaited key is eventually published.
 template <int G, int C, bool kSector>
-__global__ void __launch_bounds__(G * 32) match_queue_kernel(
+__global__ void __launch_bounds__(G * 32) match_follow_kernel(
     const __grid_constant__ MatchParams p, const int64_t* __restrict__ keys,
     const int64_t* __restrict__ key_off, int64_t n_req, int64_t* __restrict__ len_out,
-    int64_t* __restrict__ best_len, int32_t* __restrict__ best_id, const int32_t* queue,
-    unsigned long long* claim) {
+    int64_t* __restrict__ best_len, int32_t* __restrict__ best_id,
+    const int64_t* progress, const int32_t* __restrict__ order, unsigned long long* claim) {
   __shared__ long long first_miss;
   __shared__ long long req;
+  __shared__ int stop;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int64_t kWin = 32 * C;
   while (true) {
     if (threadIdx.x == 0) {
-      const unsigned long long slot = atomicAdd(claim, 1ull);
-      long long r = -1;
-      if (slot < static_cast<unsigned long long>(n_req)) {
-        unsigned ns = 64;
-        unsigned long long t0, t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-        while (true) {
-          int v;
-          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(queue + slot) : "memory");
-          if (v >= 0) {
-            r = v;
-            break;
-          }
-          __nanosleep(ns);
-          ns = ns < 2048 ? 2 * ns : ns;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-          if (t - t0 > 5000000000ull) {  // 5 s: a request never published -- report, don't hang
-            g_queue_timeouts = 1;
-            break;
-          }
-        }
-      }
-      req = r;
+      const unsigned long long pos = atomicAdd(claim, 1ull);
+      req = pos < static_cast<unsigned long long>(n_req)
+                ? (order ? static_cast<long long>(order[pos]) : static_cast<long long>(pos))
+                : -1;
+      stop = 0;
     }
     __syncthreads();
     const int64_t r = static_cast<int64_t>(req);
     if (r < 0) return;
-    for (int i = 0; i < p.n_inst; ++i)
-      match_task<G, C, kSector>(p, keys, key_off, r, i, len_out, best_len, best_id, first_miss);
+    const int64_t base = key_off[r];
+    const int64_t n = key_off[r + 1] - base;
+    const int64_t* __restrict__ q = keys + base;
+    int64_t ready = 0;  // thread 0: keys of r known to exist (relative)
+    for (int i = 0; i < p.n_inst; ++i) {
+      const int64_t t = r * p.n_inst + i;
+      const int64_t* __restrict__ tk = p.keys[i];
+      const uint64_t mask = p.mask[i];
+      if (threadIdx.x == 0) first_miss = n;
+      __syncthreads();
+      for (int64_t wave = 0;; ++wave) {
+        const int64_t need = min(n, (wave + 1) * G * kWin);
+        if (threadIdx.x == 0 && ready < need && !stop) {
+          unsigned ns = 64;
+          unsigned long long t0, tn;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          while (true) {
+            long long v;
+            asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(progress + r) : "memory");
+            ready = static_cast<int64_t>(v) - base;
+            if (ready >= need) break;
+            __nanosleep(ns);
+            ns = ns < 1024 ? 2 * ns : ns;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+            if (tn - t0 > 5000000000ull) {  // never published: report, don't hang
+              g_queue_timeouts = 1;
+              stop = 1;
+              break;
+            }
+          }
+        }
+        __syncthreads();  // the wave's keys exist (thread 0's acquire, then the barrier)
+        if (stop) break;
+        const int64_t k0 = (wave * G + warp) * kWin;
+        if (k0 < n && k0 < static_cast<int64_t>(*reinterpret_cast<volatile long long*>(&first_miss))) {
+          int64_t qk[C];
+          bool qv[C], hit[C];
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            const int64_t idx = k0 + 32 * j + lane;
+            qv[j] = idx < n;
+            // L2 only (ld.global.cg): the keys are written during this kernel
+            // by other SMs, and a line another CTA read earlier may sit stale
+            // in this SM's L1
+            qk[j] = qv[j] ? __ldcg(q + idx) : 0;
+          }
+          if (kSector) probe_sector<C>(tk, mask, qk, qv, hit);
+          else probe_multi<C>(tk, mask, qk, qv, hit);
+#pragma unroll
+          for (int j = 0; j < C; ++j) {
+            const unsigned miss = __ballot_sync(0xffffffffu, !hit[j] && qv[j]);
+            if (miss) {
+              if (lane == 0) atomicMin(&first_miss, static_cast<long long>(k0 + 32 * j + __ffs(miss) - 1));
+              break;
+            }
+          }
+        }
+        __syncthreads();
+        const int64_t fm = static_cast<int64_t>(first_miss);
+        const int64_t covered = (wave + 1) * G * kWin;
+        if (fm < covered || covered >= n) break;  // uniform over the CTA
+      }
+      if (threadIdx.x == 0 && !stop) {
+        const int64_t len = static_cast<int64_t>(first_miss);
+        match_result(p, t, r, i, len, len_out, best_len, best_id);
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -1002,12 +1054,13 @@ int match_impl(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_i
 }  // namespace
 
 namespace kvx {
-// K2 consumer of the hash's completion queue (kvx_hash_match_batch): params
-// as kvx_match_prefix_batch; launched programmatically dependent on the hash.
-int match_queue_launch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
-                       const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
-                       int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
-                       const int32_t* d_queue, unsigned long long* d_claim, void* stream) {
+// K2 following the hash's key progress (kvx_hash_match_batch): params as
+// kvx_match_prefix_batch; launched programmatically dependent on the hash.
+int match_follow_launch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
+                        const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
+                        int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
+                        const int64_t* d_progress, const int32_t* d_order,
+                        unsigned long long* d_claim, void* stream) {
   MatchParams p{};
   p.n_inst = static_cast<int32_t>(n_inst);
   const int dev = idx[0]->device;
@@ -1032,12 +1085,14 @@ int match_queue_launch(const kvx_index* const* idx, const int32_t* inst_ids, int
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (n_req * n_inst <= 1024)
-    KVX_CUDA(cudaLaunchKernelEx(&cfg, match_queue_kernel<2, 2, true>, p, d_keys, d_key_off, n_req,
-                                d_len_out, d_best_len, d_best_id, d_queue, d_claim));
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, match_follow_kernel<2, 2, true>, p, d_keys, d_key_off,
+                                n_req, d_len_out, d_best_len, d_best_id, d_progress, d_order,
+                                d_claim));
   else
-    KVX_CUDA(cudaLaunchKernelEx(&cfg, match_queue_kernel<2, 2, false>, p, d_keys, d_key_off, n_req,
-                                d_len_out, d_best_len, d_best_id, d_queue, d_claim));
-  KVX_LAUNCH_CHECK("match_queue_kernel");
+    KVX_CUDA(cudaLaunchKernelEx(&cfg, match_follow_kernel<2, 2, false>, p, d_keys, d_key_off,
+                                n_req, d_len_out, d_best_len, d_best_id, d_progress, d_order,
+                                d_claim));
+  KVX_LAUNCH_CHECK("match_follow_kernel");
   return KVX_OK;
 }
 }  // namespace kvx
@@ -1055,8 +1110,8 @@ extern "C" int kvx_hash_match_check(void* stream) {
   KVX_CUDA(cudaMemcpyFromSymbol(&t, g_queue_timeouts, sizeof(t)));
   if (!t) return KVX_OK;
   KVX_CUDA(cudaMemcpyToSymbol(g_queue_timeouts, &zero, sizeof(zero)));
-  return set_error(KVX_ECUDA, "kvx_hash_match_check: a match task waited 5 s for a request the "
-                              "hash never completed; its results are missing");
+  return set_error(KVX_ECUDA, "kvx_hash_match_check: a match task waited 5 s for keys the "
+                              "hash never published; its results are missing");
 }
 
 // ---- cross-GPU best match without a collective --------------------------
