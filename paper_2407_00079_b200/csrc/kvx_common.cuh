@@ -85,13 +85,12 @@ int copy_paged_pull(const kvx_pool* src, const int32_t* d_src_table, kvx_pool* d
                     const uint64_t* d_flag, uint64_t value, const uint64_t* d_status,
                     bool after_gate);
 int pull_done(const uint64_t* d_status, uint64_t* d_peer_flag, uint64_t value, void* stream);
-// K2 following the hash's per-request key progress (kvx_index.cu;
-// kvx_hash_match_batch); d_order: the hash's claim order (NULL: index order).
+// K2 following the hash's key production (kvx_index.cu; kvx_hash_match_batch:
+// keys preset to -1); d_order: the hash's claim order (NULL: index order).
 int match_follow_launch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
                         const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
                         int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
-                        const int64_t* d_progress, const int32_t* d_order,
-                        unsigned long long* d_claim, void* stream);
+                        const int32_t* d_order, unsigned long long* d_claim, void* stream);
 // Requests of a batch in decreasing block count (kvx_hash.cu).
 int order_by_length(const int64_t* d_key_off, int64_t n_req, int32_t* d_order,
                     unsigned long long* d_ws, cudaStream_t s);

@@ -342,19 +342,14 @@ struct alignas(16) SubDesc {
   int64_t r;      // request index
 };
 
-// Key progress per request (kvx_hash_match_batch): after the folding lane
-// stored a round's keys it publishes, with release semantics, the absolute key
-// index up to which request r's keys exist; a match kernel running beside the
-// hash follows each request's progress window by window.
+// kvx_hash_match_batch runs the hash with `enabled` set: the keys were
+// preset to -1 (no key is negative: chain_hash masks the sign bit), and a
+// match kernel beside the hash reads each key once it is no longer -1.  No
+// fence or extra store on the hash's side (a release per round would wait for
+// the round's in-flight token prefetches).
 struct Publish {
-  int64_t* progress;  // n_req entries, 0 before the first round of r
+  int enabled;
 };
-
-__device__ __forceinline__ void publish(const Publish& pub, int64_t r, int64_t key_end) {
-  __threadfence();  // the keys before the progress word
-  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(pub.progress + r), "l"(key_end)
-               : "memory");
-}
 
 // Staging of one request stream (one chain per lane) of one half-warp.
 struct HalfSmem {
@@ -390,7 +385,7 @@ __device__ __forceinline__ void claim(Cursor& c, bool need, int hl, int j, int b
                                       const int64_t* __restrict__ key_off, int64_t n_req,
                                       const int32_t* __restrict__ order,
                                       unsigned long long* ctr, unsigned long long& first,
-                                      unsigned long long base, const Publish* pub = nullptr) {
+                                      unsigned long long base) {
   while (__any_sync(0xffffffffu, need)) {
     unsigned long long idx = 0;
     if (need && first != ~0ull) {
@@ -818,7 +813,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
     int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
     const int32_t* __restrict__ order, unsigned long long* ctr, int prio, Publish pubv) {
-  const Publish* pub = pubv.progress ? &pubv : nullptr;
+  (void)pubv;
   extern __shared__ __align__(16) unsigned char hw_smem_raw[];
   WarpSmem<1>& S = reinterpret_cast<WarpSmem<1>*>(hw_smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -848,22 +843,20 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
   P.prem = P.ntok = P.nblk = P.k = P.u = P.m = 0;
   P.kb0 = 0;
   P.r = 0;
-  claim(P, true, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base, pub);
+  claim(P, true, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
 #pragma unroll 1
   for (int i = 0; i < kPrefetch; ++i) {
     if (kLazyIssue) issue_p(P, H, i, hl, j, bs, nsub, tokens);
     else issue_p0(P, H, i, hl, j, bs, nsub, tokens);
     const bool need = step_cursor_p(P, bs, nsub);
     if (__any_sync(0xffffffffu, need))
-      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base, pub);
+      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
   }
   // sub-round 0's tokens and control
   asm volatile("cp.async.wait_group %0;" ::"n"(kPrefetch - 1) : "memory");
   __syncwarp();
   int fn = 0, freset = 0;  // folds of the current sub-round (the previous round's blocks)
   int64_t fkb = 0;
-  int64_t fold_r = -1;     // request whose round the folder folds in this sub-round
-  int64_t fold_end = 0;    // ... and the absolute key index that round ends at
   Ctl c = make_ctl(H, S.zero, 0, folder, j, bs, 0);
   int64_t h = 0;
 #pragma unroll 1
@@ -916,16 +909,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
       H.clo[j] = static_cast<uint32_t>(h);
       H.chi[j] = static_cast<uint32_t>(static_cast<uint64_t>(h) >> 32);
     }
-    // the folder just stored the keys of a round of request fold_r
-    if (pub && folder && fold_r >= 0) publish(*pub, fold_r, fold_end);
-    fold_r = round_done ? c.r : -1;
-    fold_end = c.kb + c.nb;
+
     fn = fn_next;
     fkb = c.kb;
     freset = c.flags & 4;
     __syncwarp();
     if (__any_sync(0xffffffffu, need))
-      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base, pub);
+      claim(P, need, hl, j, bs, tokens, tok_off, key_off, n_req, order, ctr, first, base);
     c = cn;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1015,6 +1005,18 @@ __global__ void __launch_bounds__(kScanThreads) key_offsets_kernel(
 }  // namespace kvx
 
 namespace kvx {
+namespace {
+// keys[key_off[0] .. key_off[n_req]) = -1 (the batch's key range, read on the device).
+__global__ void __launch_bounds__(256) keys_unset_kernel(const int64_t* __restrict__ key_off,
+                                                         int64_t n_req, int64_t* keys) {
+  const int64_t first = key_off[0], last = key_off[n_req];
+  for (int64_t i = first + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < last;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    keys[i] = -1;
+}
+
+}  // namespace
+
 // Requests in decreasing block count (the hash's counting sort), for kernels
 // that schedule long requests first (the prefix match); ws: one u64 of scratch.
 int order_by_length(const int64_t* d_key_off, int64_t n_req, int32_t* d_order,
@@ -1051,7 +1053,7 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
                                     int64_t* d_keys, void* stream) {
   bool published = false;
   return hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream,
-                     hw::Publish{nullptr}, &published);
+                     hw::Publish{0}, &published);
 }
 
 namespace {
@@ -1169,7 +1171,7 @@ int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req
                                              : hw::halfwarp_hash_kernel_p<false>,
                                   d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
                                   static_cast<const int32_t*>(order), ctr, order ? prio : 0, pub));
-      *published = pub.progress != nullptr;
+      *published = pub.enabled != 0;
       if (order_used) *order_used = order;
     } else {
       KVX_CUDA(cudaLaunchKernelEx(&cfg,
@@ -1202,11 +1204,9 @@ int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req
   return KVX_OK;
 }
 
-// Progress words + the consumer's claim counter per (device, stream).
+// The follower's claim counter per (device, stream).
 struct QueueScratch {
-  int64_t* progress = nullptr;
   unsigned long long* ctr = nullptr;
-  int64_t cap = 0;
 };
 std::mutex g_queue_mu;
 std::map<std::pair<int, void*>, QueueScratch> g_queues;
@@ -1215,10 +1215,10 @@ std::map<std::pair<int, void*>, QueueScratch> g_queues;
 // Stage 1 in one stream-ordered call: the block hash, and the prefix match of
 // each request following the hash's key production window by window (a
 // match kernel resident beside the hash takes the requests in the hash's
-// longest-first order and waits per window for the request's published key
-// progress).  A prefix match ends at the first miss, typically long before
-// the request's last key exists, so the match of the batch hides under the
-// hash instead of following it.  Results are those of kvx_chain_hash_batch followed by
+// longest-first order and reads a window's keys once none is still the -1
+// they were preset to).  A prefix match ends at the first miss, typically
+// long before the request's last key exists, so the match of the batch hides
+// under the hash instead of following it.  Results are those of kvx_chain_hash_batch followed by
 // kvx_match_prefix_batch; block sizes the half-warp kernel does not take run
 // exactly that sequence.
 extern "C" int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_tok_off,
@@ -1241,31 +1241,24 @@ extern "C" int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_to
   {
     std::lock_guard<std::mutex> lk(g_queue_mu);
     q = &g_queues[{dev, stream}];
-    if (q->cap < n_req) {
-      if (q->progress) KVX_CUDA(cudaFree(q->progress));  // cudaFree waits for the device
-      q->progress = nullptr;
-      q->cap = 0;
-      const int64_t cap = std::max<int64_t>(n_req, 4096);
-      KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&q->progress), (cap + 8) * sizeof(int64_t)));
-      q->ctr = reinterpret_cast<unsigned long long*>(q->progress + cap);
-      q->cap = cap;
-    }
+    if (!q->ctr) KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&q->ctr), 64));
   }
-  // progress 0 = no key yet; the claim counter 0
-  KVX_CUDA(cudaMemsetAsync(q->progress, 0, n_req * sizeof(int64_t), s));
   KVX_CUDA(cudaMemsetAsync(q->ctr, 0, sizeof(unsigned long long), s));
+  // every key -1 until the hash stores it (the follower's readiness test)
+  keys_unset_kernel<<<sm_count(dev) * 4, 256, 0, s>>>(d_key_off, n_req, d_keys);
+  KVX_LAUNCH_CHECK("keys_unset_kernel");
   if (d_best_len && n_inst > 1)  // the packed atomicMax words start at 0
     KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
   bool published = false;
   const int32_t* order = nullptr;
   int rc = hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream,
-                       hw::Publish{q->progress}, &published, &order);
+                       hw::Publish{1}, &published, &order);
   if (rc) return rc;
   if (!published)  // the producer / fold kernel (bs % 16 != 0): hash, then match
     return kvx_match_prefix_batch(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out,
                                   d_best_len, d_best_id, stream);
   rc = match_follow_launch(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out,
-                           d_best_len, d_best_id, q->progress, order, q->ctr, stream);
+                           d_best_len, d_best_id, order, q->ctr, stream);
   if (rc) return rc;
   if (d_best_len && n_inst > 1)
     return kvx_best_unpack(reinterpret_cast<const uint64_t*>(d_best_len), n_req, d_best_len,

@@ -512,18 +512,20 @@ __global__ void __launch_bounds__(G * 32, MINB) match_group_kernel(
 __device__ unsigned long long g_queue_timeouts = 0;
 
 // K2 following the block hash running beside it (kvx_hash_match_batch).  A
-// CTA takes requests in the hash's own longest-first claim order and, before
-// each wave, waits (thread 0: acquire loads of the request's published key
-// progress, back-off, 5 s limit) until the wave's keys exist.  The match stops
-// at the first miss, usually long before the request's hash ends.  Launched
-// programmatically dependent on the hash, which triggers only once all of its
-// CTAs are resident, so every awaited key is eventually published.
+// CTA takes requests in the hash's own longest-first claim order; each warp
+// loads its window's keys from L2 and re-polls (back-off, 5 s limit) the ones
+// that are still -1, the value the keys were preset to -- no key is negative,
+// and each 8-byte key is stored whole -- so a window is probed as soon as the
+// hash has produced it.  The match stops at the first miss, usually long
+// before the request's hash ends.  Launched programmatically dependent on the
+// hash, which triggers only once all of its CTAs are resident, so every
+// awaited key is eventually stored.
 template <int G, int C, bool kSector>
 __global__ void __launch_bounds__(G * 32) match_follow_kernel(
     const __grid_constant__ MatchParams p, const int64_t* __restrict__ keys,
     const int64_t* __restrict__ key_off, int64_t n_req, int64_t* __restrict__ len_out,
     int64_t* __restrict__ best_len, int32_t* __restrict__ best_id,
-    const int64_t* progress, const int32_t* __restrict__ order, unsigned long long* claim) {
+    const int32_t* __restrict__ order, unsigned long long* claim) {
   __shared__ long long first_miss;
   __shared__ long long req;
   __shared__ int stop;
@@ -542,8 +544,7 @@ __global__ void __launch_bounds__(G * 32) match_follow_kernel(
     if (r < 0) return;
     const int64_t base = key_off[r];
     const int64_t n = key_off[r + 1] - base;
-    const int64_t* __restrict__ q = keys + base;
-    int64_t ready = 0;  // thread 0: keys of r known to exist (relative)
+    const int64_t* q = keys + base;
     for (int i = 0; i < p.n_inst; ++i) {
       const int64_t t = r * p.n_inst + i;
       const int64_t* __restrict__ tk = p.keys[i];
@@ -551,40 +552,43 @@ __global__ void __launch_bounds__(G * 32) match_follow_kernel(
       if (threadIdx.x == 0) first_miss = n;
       __syncthreads();
       for (int64_t wave = 0;; ++wave) {
-        const int64_t need = min(n, (wave + 1) * G * kWin);
-        if (threadIdx.x == 0 && ready < need && !stop) {
-          unsigned ns = 64;
-          unsigned long long t0, tn;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-          while (true) {
-            long long v;
-            asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(progress + r) : "memory");
-            ready = static_cast<int64_t>(v) - base;
-            if (ready >= need) break;
-            __nanosleep(ns);
-            ns = ns < 1024 ? 2 * ns : ns;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
-            if (tn - t0 > 5000000000ull) {  // never published: report, don't hang
-              g_queue_timeouts = 1;
-              stop = 1;
-              break;
-            }
-          }
-        }
-        __syncthreads();  // the wave's keys exist (thread 0's acquire, then the barrier)
-        if (stop) break;
         const int64_t k0 = (wave * G + warp) * kWin;
         if (k0 < n && k0 < static_cast<int64_t>(*reinterpret_cast<volatile long long*>(&first_miss))) {
           int64_t qk[C];
           bool qv[C], hit[C];
+          // L2 only (ld.global.cg): the keys are stored during this kernel by
+          // other SMs, and a line read earlier may sit stale in this SM's L1
 #pragma unroll
           for (int j = 0; j < C; ++j) {
             const int64_t idx = k0 + 32 * j + lane;
             qv[j] = idx < n;
-            // L2 only (ld.global.cg): the keys are written during this kernel
-            // by other SMs, and a line another CTA read earlier may sit stale
-            // in this SM's L1
             qk[j] = qv[j] ? __ldcg(q + idx) : 0;
+          }
+          bool pending = false;
+#pragma unroll
+          for (int j = 0; j < C; ++j) pending = pending || qk[j] < 0;
+          if (__any_sync(0xffffffffu, pending)) {
+            unsigned ns = 64;
+            unsigned long long t0, tn;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (__any_sync(0xffffffffu, pending)) {
+              __nanosleep(ns);
+              ns = ns < 1024 ? 2 * ns : ns;
+              pending = false;
+#pragma unroll
+              for (int j = 0; j < C; ++j) {
+                if (qk[j] < 0) qk[j] = __ldcg(q + k0 + 32 * j + lane);
+                pending = pending || qk[j] < 0;
+              }
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+              if (tn - t0 > 5000000000ull) {  // never stored: report, don't hang
+                if (lane == 0) {
+                  g_queue_timeouts = 1;
+                  stop = 1;
+                }
+                break;
+              }
+            }
           }
           if (kSector) probe_sector<C>(tk, mask, qk, qv, hit);
           else probe_multi<C>(tk, mask, qk, qv, hit);
@@ -600,13 +604,14 @@ __global__ void __launch_bounds__(G * 32) match_follow_kernel(
         __syncthreads();
         const int64_t fm = static_cast<int64_t>(first_miss);
         const int64_t covered = (wave + 1) * G * kWin;
-        if (fm < covered || covered >= n) break;  // uniform over the CTA
+        if (stop || fm < covered || covered >= n) break;  // uniform over the CTA
       }
       if (threadIdx.x == 0 && !stop) {
         const int64_t len = static_cast<int64_t>(first_miss);
         match_result(p, t, r, i, len, len_out, best_len, best_id);
       }
       __syncthreads();
+      if (stop) break;
     }
   }
 }
@@ -1059,8 +1064,7 @@ namespace kvx {
 int match_follow_launch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
                         const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
                         int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
-                        const int64_t* d_progress, const int32_t* d_order,
-                        unsigned long long* d_claim, void* stream) {
+                        const int32_t* d_order, unsigned long long* d_claim, void* stream) {
   MatchParams p{};
   p.n_inst = static_cast<int32_t>(n_inst);
   const int dev = idx[0]->device;
@@ -1086,12 +1090,10 @@ int match_follow_launch(const kvx_index* const* idx, const int32_t* inst_ids, in
   cfg.numAttrs = 1;
   if (n_req * n_inst <= 1024)
     KVX_CUDA(cudaLaunchKernelEx(&cfg, match_follow_kernel<2, 2, true>, p, d_keys, d_key_off,
-                                n_req, d_len_out, d_best_len, d_best_id, d_progress, d_order,
-                                d_claim));
+                                n_req, d_len_out, d_best_len, d_best_id, d_order, d_claim));
   else
     KVX_CUDA(cudaLaunchKernelEx(&cfg, match_follow_kernel<2, 2, false>, p, d_keys, d_key_off,
-                                n_req, d_len_out, d_best_len, d_best_id, d_progress, d_order,
-                                d_claim));
+                                n_req, d_len_out, d_best_len, d_best_id, d_order, d_claim));
   KVX_LAUNCH_CHECK("match_follow_kernel");
   return KVX_OK;
 }
