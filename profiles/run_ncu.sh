@@ -19,6 +19,6 @@ ncu --set full --clock-control none --import-source on -k regex:copy_lsu -s 250 
 
 # 3. full set on the stage-1 kernels (block hash + prefix match, Config 4 batch)
 python bench.py $MATCH > gpurun_out/ncu_plain_match.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"hash_kernel|match_group|match_kernel" \
-    -s 3 -c 3 -o gpurun_out/prof_match_${TAG} python bench.py $MATCH > gpurun_out/ncu_match.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"hash_kernel|match_group|match_kernel|match_follow" \
+    -s 3 -c 4 -o gpurun_out/prof_match_${TAG} python bench.py $MATCH > gpurun_out/ncu_match.log 2>&1
 echo done
