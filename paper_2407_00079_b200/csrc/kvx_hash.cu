@@ -921,415 +921,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// ---- K1d: per-SM content producers + one key-folding lane per request ------
-//
-// The half-warp kernel's batch time is set by its longest key chains: a
-// 1,536-block request runs its 1,648 half-warp steps at ~145 cycles each
-// (the chain plus the half-warp's own bookkeeping, on a sub-partition shared
-// with two other warps), while the whole batch's hashing fits in ~0.65 of
-// that time.  K1d separates the two again, inside one SM: each CTA (one per
-// SM) owns up to 32 requests per generation -- longest-first positions dealt
-// serpentine over the SMs, so every SM gets the same mix -- and
-//   * producer warps hash block contents, one 32-block window of one request
-//     per task (lane = block; the next task's tokens are copied into the
-//     warp's shared-memory buffer by cp.async while the current task is
-//     hashed), into a shared-memory ring of kFoldRing windows per request,
-//     and publish each window with a flag.  A task is handed out only when
-//     its ring slot is free, to the request with the most windows left, so
-//     the longest key chains are fed first and no producer ever waits on
-//     the fold;
-//   * one folding warp (the highest warp id: its sub-partition's scheduler
-//     issues it first) folds all of the CTA's requests at once, lane =
-//     request, a window at a time as soon as its flag is set -- the serial
-//     key chain runs at the chain_hash latency and never waits on L2.
-constexpr int kFoldWin = 32;     // blocks per window (one producer task)
-constexpr int kFoldRing = 8;     // windows per request in the ring
-constexpr int kFoldLanes = 32;   // requests per CTA per generation
-#ifndef KVX_HASH_FOLD_WARPS_PER_CTA
-#define KVX_HASH_FOLD_WARPS_PER_CTA 28  // 7 per SM sub-partition
-#endif
-#ifndef KVX_HASH_FOLD_SHARE
-#define KVX_HASH_FOLD_SHARE 1  // producer warps beside the folding warp on its sub-partition
-#endif
-constexpr int kMaxFoldCtaWarps = 28;  // 72 registers per thread
-constexpr int kTokWords = 20;      // one 16-token chunk + misalignment, per lane
-constexpr int kMailEmpty = -1, kMailDone = -2;
-
-struct FoldSmem {
-  int64_t ring[kFoldRing][kFoldWin][kFoldLanes];  // [slot][block][request lane]: 64 KB
-  int64_t kb0[kFoldLanes], tb0[kFoldLanes];
-  int ntok[kFoldLanes], nblk[kFoldLanes], nw[kFoldLanes];
-  int mail[kMaxFoldCtaWarps];        // per producer warp: next task (w << 5 | lane), or empty / done
-  int ready[kFoldLanes][kFoldRing];  // window index + 1 once stored
-  int folded[kFoldLanes];            // windows folded
-  // followed by the producers' token buffers: [warp][2][lane][kTokWords]
-};
-__host__ __device__ constexpr size_t fold_smem_bytes(int warps) {
-  return sizeof(FoldSmem) + static_cast<size_t>(warps - 1) * 2 * kFoldWin * kTokWords * 4;
-}
-
-__device__ __forceinline__ int lds_volatile(const int* p) {
-  return *reinterpret_cast<const volatile int*>(p);
-}
-__device__ __forceinline__ void sts_volatile(int* p, int v) {
-  *reinterpret_cast<volatile int*>(p) = v;
-}
-
-// A producer task: window w of the request in fold lane `ln`.
-struct FoldTask {
-  int ln, w;
-  bool valid;  // a task was handed out
-  bool done;   // every window of the generation is handed out
-};
-// This lane's block of a task.
-struct FoldBlk {
-  int64_t t;  // first token
-  int rem;    // tokens from t to the request end (<= 0: no block)
-  int M;      // misalignment of the request's tokens (bs % 16 == 0: shared by its blocks);
-              // a chunk's 16 tokens are words M .. M + 15 of the lane's row
-};
-
-template <int kFoldPass>
-__global__ void __launch_bounds__(kMaxFoldCtaWarps * 32, 1) lane_fold_hash_kernel(
-    const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
-    int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
-    const int32_t* __restrict__ order, int fold_share, int prio_key, unsigned long long* prof) {
-  extern __shared__ __align__(16) unsigned char lf_smem_raw[];
-  // prof (measurement only, KVX_HASH_PROFILE=1): cycles per phase, summed
-  // over warps -- producers: claim, issue, wait, hash, publish; folder:
-  // idle, windows
-  unsigned long long acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  long long t_last = prof ? clock64() : 0;
-  auto tick = [&](int sec) {
-    if (prof) {
-      const long long t = clock64();
-      acc[sec] += static_cast<unsigned long long>(t - t_last);
-      t_last = t;
-    }
-  };
-  FoldSmem& S = *reinterpret_cast<FoldSmem*>(lf_smem_raw);
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  // The folding warp is the highest warp id; its SM sub-partition (warp id
-  // mod 4) runs only `fold_share` producers beside it -- the scheduler's
-  // priority alone does not keep a saturated sub-partition from stretching
-  // the fold's dependent chain (~260 instead of ~120 cycles per block with
-  // six producers there) -- the other warps on it stay idle.
-  const int fold_warp = static_cast<int>(blockDim.x >> 5) - 1;
-  const bool folder = warp == fold_warp;
-  const bool producer =
-      !folder && ((warp & 3) != (fold_warp & 3) || (warp >> 2) < fold_share);
-  // the dispatcher: the next warp id on the folding warp's sub-partition
-  const bool dispatcher = warp == fold_warp - 4 && !producer;
-  const int nsub = bs >> 4;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-
-  const int64_t G = static_cast<int64_t>(gridDim.x) * kFoldLanes;
-  for (int64_t g0 = 0; g0 < n_req; g0 += G) {
-    if (folder) {
-      // this CTA's requests of the generation: positions dealt serpentine
-      const int64_t pos = g0 + static_cast<int64_t>(lane) * gridDim.x +
-                          ((lane & 1) ? gridDim.x - 1 - blockIdx.x : blockIdx.x);
-      int nb = 0;
-      if (pos < n_req) {
-        const int64_t r = order ? static_cast<int64_t>(order[pos]) : pos;
-        S.kb0[lane] = key_off[r];
-        S.tb0[lane] = tok_off[r];
-        S.ntok[lane] = static_cast<int>(tok_off[r + 1] - tok_off[r]);
-        nb = static_cast<int>(key_off[r + 1] - key_off[r]);
-      }
-      S.nblk[lane] = nb;
-      S.nw[lane] = (nb + kFoldWin - 1) / kFoldWin;
-      S.mail[lane] = kMailEmpty;
-      S.folded[lane] = 0;
-#pragma unroll
-      for (int k = 0; k < kFoldRing; ++k) S.ready[lane][k] = 0;
-    }
-    __syncthreads();
-
-    if (producer) {
-      // ---- producers ----
-      uint32_t(*tb)[kFoldWin][kTokWords] = reinterpret_cast<uint32_t(*)[kFoldWin][kTokWords]>(
-          lf_smem_raw + sizeof(FoldSmem)) + 2 * warp;  // this warp's two buffers
-      // Tasks arrive in this warp's mailbox from the dispatcher warp.
-      auto claim = [&](bool wait) {
-        FoldTask k;
-        k.valid = k.done = false;
-        unsigned ns = 32;
-        int v = kMailEmpty;
-        if (lane == 0) {
-          while ((v = lds_volatile(&S.mail[warp])) == kMailEmpty && wait) {
-            __nanosleep(ns);
-            ns = ns < 256 ? ns * 2 : ns;
-          }
-          if (v >= 0) sts_volatile(&S.mail[warp], kMailEmpty);  // taken: the dispatcher refills
-        }
-        v = __shfl_sync(0xffffffffu, v, 0);
-        if (v == kMailDone) k.done = true;
-        if (v >= 0) {
-          k.valid = true;
-          k.ln = v & (kFoldLanes - 1);
-          k.w = v >> 5;
-        }
-        return k;
-      };
-      auto blk_of = [&](const FoldTask& k) {
-        FoldBlk b;
-        const int64_t tb0 = S.tb0[k.ln];
-        const int blkno = k.w * kFoldWin + lane;
-        b.t = tb0 + static_cast<int64_t>(blkno) * bs;
-        b.rem = blkno < S.nblk[k.ln] ? S.ntok[k.ln] - blkno * bs : 0;
-        b.M = static_cast<int>(tb0 & 3);
-        return b;
-      };
-      // cp.async chunk ci of the lane's block into buffer `buf` (bytes past
-      // the request's last token are not copied and never read)
-      auto issue = [&](int buf, const FoldBlk& b, int ci) {
-        const int left = b.rem - 16 * ci;
-        const int prem = left + b.M;  // words from the aligned start to the request end
-        const int32_t* a = tokens + (b.t + 16 * ci - b.M);
-        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tb[buf][lane][0]));
-        if (__all_sync(0xffffffffu, left <= 0 || prem >= kTokWords)) {  // whole rows
-#pragma unroll
-          for (int q = 0; q < 5; ++q) cp_async16_pred(dst + 16 * q, a + 4 * q, 16, left > 0);
-        } else {  // a request's last blocks: stop at its last token
-#pragma unroll
-          for (int q = 0; q < 5; ++q) {
-            const int bytes = max(0, min(4, prem - 4 * q)) * 4;
-            const bool on = left > 0 && bytes > 0;
-            cp_async16_pred(dst + 16 * q, on ? static_cast<const void*>(a + 4 * q)
-                                             : static_cast<const void*>(tokens),
-                            bytes, on);
-          }
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-      };
-      // the chunk's 16 tokens start M words into the lane's row: one code
-      // path for every alignment (a switch over M would quadruple the hot
-      // loop's code, and warps of one sub-partition hashing requests of
-      // different alignments would then share the instruction cache)
-      auto hash_buf = [&](int buf, const FoldBlk& b, int ci, int64_t h) {
-        const uint32_t* src = &tb[buf][lane][b.M];
-        const int left = b.rem - 16 * ci;
-        const int n = left < 0 ? 0 : (left > 16 ? 16 : left);
-        if (__all_sync(0xffffffffu, n == 16 || b.rem <= 0)) {
-#pragma unroll
-          for (int s = 0; s < 16; ++s) h = chain_hash(h, static_cast<uint64_t>(src[s]));
-        } else {
-#pragma unroll
-          for (int s = 0; s < 16; ++s) {
-            const int64_t hn = chain_hash(h, static_cast<uint64_t>(src[s]));
-            h = s < n ? hn : h;
-          }
-        }
-        return h;
-      };
-      auto publish = [&](const FoldTask& k, const FoldBlk& b, int64_t content) {
-        if (prof && blockIdx.x == 0 && lane == 0) {
-          const unsigned long long e = atomicAdd(prof + 8, 1ull);
-          if (e < 4000) {
-            prof[16 + 2 * e] = static_cast<unsigned long long>(clock64());
-            prof[17 + 2 * e] = (2ull << 60) | (static_cast<unsigned long long>(k.ln) << 16) | k.w;
-          }
-        }
-        const int slot = k.w % kFoldRing;
-        if (b.rem > 0) S.ring[slot][lane][k.ln] = content;
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence_block();
-          sts_volatile(&S.ready[k.ln][slot], k.w + 1);
-        }
-      };
-
-      FoldTask cur = claim(true);
-      tick(0);
-      if (cur.valid) {
-        FoldBlk bc = blk_of(cur);
-        int ci = 0, buf = 0;
-        int64_t h = 0;
-        issue(0, bc, 0);
-        tick(1);
-        while (true) {
-          // the next chunk (this block's next one, or the next task's first)
-          // is copied while this one is hashed
-          FoldTask nt = cur;
-          FoldBlk nb = bc;
-          int nci = ci + 1;
-          bool pending = false;  // next task still to be claimed (no room right now)
-          if (nci < nsub) {
-            issue(buf ^ 1, bc, nci);
-            tick(1);
-          } else {
-            nci = 0;
-            nt = claim(false);
-            tick(0);
-            if (nt.valid) {
-              nb = blk_of(nt);
-              issue(buf ^ 1, nb, 0);
-            } else {
-              pending = !nt.done;
-              asm volatile("cp.async.commit_group;" ::: "memory");
-            }
-            tick(1);
-          }
-          asm volatile("cp.async.wait_group 1;" ::: "memory");
-          tick(2);
-          h = hash_buf(buf, bc, ci, h);
-          tick(3);
-          if (ci + 1 == nsub) {
-            publish(cur, bc, h);
-            h = 0;
-            tick(4);
-            if (pending) {
-              nt = claim(true);
-              tick(0);
-              if (nt.valid) {
-                nb = blk_of(nt);
-                issue(buf ^ 1, nb, 0);
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-              }
-              tick(2);
-            }
-            if (!nt.valid) break;
-          }
-          cur = nt;
-          bc = nb;
-          ci = nci;
-          buf ^= 1;
-        }
-      }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-    } else if (dispatcher) {
-      // ---- the dispatcher: fills empty producer mailboxes with the next
-      // window of the most critical request whose ring has room -- the
-      // request with the most windows left to produce, then the one with the
-      // fewest already waiting (lane = request for the priority, lane =
-      // producer warp for the mailboxes) ----
-      const int nw = S.nw[lane];
-      int p = 0;  // windows of request `lane` handed out
-      const bool prod_lane = lane < fold_warp && ((lane & 3) != (fold_warp & 3) ||
-                                                  (lane >> 2) < fold_share);
-      unsigned ns = 32;
-      int left = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(nw));
-      unsigned pending_done = __ballot_sync(0xffffffffu, prod_lane);
-      while (pending_done) {
-        const bool empty = ((pending_done >> lane) & 1) && lds_volatile(&S.mail[lane]) == kMailEmpty;
-        unsigned em = __ballot_sync(0xffffffffu, empty);
-        if (!em) {
-          __nanosleep(ns);
-          ns = ns < 128 ? ns * 2 : ns;
-          continue;
-        }
-        ns = 32;
-        const int f = lds_volatile(&S.folded[lane]);
-        while (em) {
-          const int m = __ffs(em) - 1;
-          em &= em - 1;
-          if (left == 0) {  // all handed out: this producer is done
-            if (lane == 0) sts_volatile(&S.mail[m], kMailDone);
-            pending_done &= ~(1u << m);
-            continue;
-          }
-          const unsigned key = (p < nw && p < f + kFoldRing)
-                                   ? (static_cast<unsigned>(nw - p) << 8) |
-                                         static_cast<unsigned>(255 - (p - f))
-                                   : 0u;
-          const unsigned best = __reduce_max_sync(0xffffffffu, key);
-          if (best == 0) {  // every request with windows left has a full ring
-            __nanosleep(64);
-            break;
-          }
-          const int ln = __ffs(__ballot_sync(0xffffffffu, key == best)) - 1;
-          if (lane == ln) {
-            sts_volatile(&S.mail[m], (p << 5) | ln);
-            ++p;
-          }
-          --left;
-        }
-      }
-      (void)prio_key;
-    } else if (folder) {
-      // ---- the folding warp: lane = request ----
-      // Passes of 8 blocks: every lane whose current window is published
-      // folds its next 8 blocks (contents loaded up front, so the chain never
-      // waits on shared memory); a window that lands mid-pass is taken up at
-      // the next pass, 8 steps later.
-      const int nb = S.nblk[lane];
-      int64_t* dst = keys + S.kb0[lane];
-      int i = 0;      // blocks folded
-      int avail = 0;  // published blocks of the current window not yet folded
-      int64_t h = 0;
-      unsigned ns = 32;
-      while (__any_sync(0xffffffffu, i < nb)) {
-        if (avail == 0 && i < nb) {
-          const int w = i / kFoldWin;
-          if (lds_volatile(&S.ready[lane][w % kFoldRing]) == w + 1) {
-            __threadfence_block();
-            avail = min(kFoldWin, nb - i);
-          }
-        }
-        const bool act = avail > 0;
-        if (!__any_sync(0xffffffffu, act)) {
-          __nanosleep(ns);
-          ns = ns < 256 ? ns * 2 : ns;
-          tick(5);
-          continue;
-        }
-        ns = 32;
-        if (prof && blockIdx.x == 0) {
-          const unsigned m = __ballot_sync(0xffffffffu, act);
-          if (lane == 0) {
-            const unsigned long long e = atomicAdd(prof + 8, 1ull);
-            if (e < 4000) {
-              prof[16 + 2 * e] = static_cast<unsigned long long>(clock64());
-              prof[17 + 2 * e] = (1ull << 60) | m;
-            }
-          }
-        }
-        const bool whole = __all_sync(0xffffffffu, !act || avail >= kFoldPass);
-        if (act) {
-          const int w = i / kFoldWin;
-          const int64_t* src = &S.ring[w % kFoldRing][i % kFoldWin][lane];
-          int n = kFoldPass;
-          if (whole) {
-#pragma unroll
-            for (int k = 0; k < kFoldPass; ++k) {
-              h = chain_hash(h, static_cast<uint64_t>(src[k * kFoldLanes]));
-              dst[i + k] = h;
-            }
-          } else {
-            n = min(kFoldPass, avail);
-#pragma unroll
-            for (int k = 0; k < kFoldPass; ++k) {
-              const int64_t hn = chain_hash(h, static_cast<uint64_t>(src[k * kFoldLanes]));
-              if (k < n) {
-                h = hn;
-                dst[i + k] = h;
-              }
-            }
-          }
-          i += n;
-          avail -= n;
-          if (avail == 0) {
-            __threadfence_block();
-            sts_volatile(&S.folded[lane], w + 1);
-          }
-        }
-        tick(6);
-        if (prof && lane == 0) acc[7] += 1;  // passes
-      }
-    }
-    __syncthreads();  // the generation's ring and request table are reused
-  }
-  if (prof && lane == 0) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) atomicAdd(prof + k, acc[k]);
-    atomicAdd(prof + 10, acc[8]);
-    atomicAdd(prof + 11, acc[9]);
-  }
-}
-
 }  // namespace hw
 
 // Claim counters and the longest-first order are per (device, stream):
@@ -1346,7 +937,6 @@ struct Workspace {
   std::map<std::pair<int, void*>, Scratch> scratch;
   int grid[64] = {0};
   bool hw_attr[64] = {false};
-  bool lf_attr[64] = {false};
 };
 
 Workspace& workspace() {
@@ -1450,7 +1040,6 @@ extern "C" int kvx_key_offsets(const int64_t* d_tok_off, int64_t n_req, int64_t 
 }
 
 namespace {
-unsigned long long* g_lf_prof = nullptr;  // KVX_HASH_PROFILE scratch (one device)
 // The block hash; with pub.queue set (half-warp kernel only) every request is
 // appended to the completion queue once its keys are stored.  *published
 // reports whether the launched kernel publishes.
@@ -1576,54 +1165,6 @@ int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req
       const char* e = std::getenv("KVX_HASH_ISSUE");  // 0: per-chunk sizes every sub-round
       return !(e && e[0] == '0');
     }();
-    const bool lane_fold = kern && std::strcmp(kern, "fold") == 0;  // K1d
-    if (lane_fold) {
-      static const int fwarps = [] {
-        const char* e = std::getenv("KVX_HASH_FOLD_CTA_WARPS");  // tuning knob
-        const int w = e ? std::atoi(e) : KVX_HASH_FOLD_WARPS_PER_CTA;
-        return std::max(2, std::min(w, hw::kMaxFoldCtaWarps));
-      }();
-      static const int fshare = [] {
-        const char* e = std::getenv("KVX_HASH_FOLD_SHARE");  // tuning knob
-        return e ? std::atoi(e) : KVX_HASH_FOLD_SHARE;
-      }();
-      static const int fpass = [] {
-        const char* e = std::getenv("KVX_HASH_FOLD_PASS");  // tuning knob: 8, 16 or 32
-        const int v = e ? std::atoi(e) : 32;
-        return v == 8 ? 8 : (v == 16 ? 16 : 32);
-      }();
-      static const int pkey = [] {
-        const char* e = std::getenv("KVX_HASH_PRIO_KEY");  // 0: windows left to produce, 1: to fold
-        return e ? std::atoi(e) : 0;
-      }();
-      auto kfn = fpass == 8 ? hw::lane_fold_hash_kernel<8>
-                            : (fpass == 16 ? hw::lane_fold_hash_kernel<16> : hw::lane_fold_hash_kernel<32>);
-      if (!W.lf_attr[dev]) {
-        for (auto f : {hw::lane_fold_hash_kernel<8>, hw::lane_fold_hash_kernel<16>,
-                       hw::lane_fold_hash_kernel<32>})
-          KVX_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(hw::fold_smem_bytes(hw::kMaxFoldCtaWarps))));
-        W.lf_attr[dev] = true;
-      }
-      cfg.blockDim = dim3(fwarps * 32);
-      cfg.dynamicSmemBytes = hw::fold_smem_bytes(fwarps);
-      unsigned long long* prof = nullptr;
-      if (const char* e = std::getenv("KVX_HASH_PROFILE")) {  // measurement only
-        if (e[0] == '1') {
-          if (!g_lf_prof) {
-            KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&g_lf_prof), 8 * 8016));
-            KVX_CUDA(cudaMemset(g_lf_prof, 0, 8 * 8016));
-          }
-          prof = g_lf_prof;
-        }
-      }
-      KVX_CUDA(cudaLaunchKernelEx(&cfg, kfn, d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
-                                  static_cast<const int32_t*>(order), fshare, pkey, prof));
-      KVX_LAUNCH_CHECK("lane_fold_hash_kernel");
-      *published = pub.enabled != 0;
-      if (order_used) *order_used = order;
-      return KVX_OK;
-    }
     if (pipelined) {
       KVX_CUDA(cudaLaunchKernelEx(&cfg,
                                   lazy_issue ? hw::halfwarp_hash_kernel_p<true>
@@ -1663,21 +1204,6 @@ int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req
   return KVX_OK;
 }
 
-}  // namespace
-
-// Measurement only (KVX_HASH_PROFILE=1, K1d): the phase cycle sums of the
-// launches since the last reset, then an event trace of SM 0 ([8] = count,
-// [16 + 2e] = clock, [17 + 2e] = event); out must hold 8,016 words -- not
-// part of the public ABI.
-extern "C" int kvx_hash_profile(unsigned long long* out8, int reset) {
-  if (!g_lf_prof) return KVX_OK;
-  KVX_CUDA(cudaDeviceSynchronize());
-  if (out8) KVX_CUDA(cudaMemcpy(out8, g_lf_prof, 8 * 8016, cudaMemcpyDeviceToHost));
-  if (reset) KVX_CUDA(cudaMemset(g_lf_prof, 0, 8 * 8016));
-  return KVX_OK;
-}
-
-namespace {
 // The follower's claim counter per (device, stream).
 struct QueueScratch {
   unsigned long long* ctr = nullptr;

@@ -41,7 +41,7 @@ for _ in range(runs):
 e1.record()
 torch.cuda.synchronize()
 f(buf, 0)
-v = [int(x) for x in buf[:12]]
+v = [int(x) for x in buf[:14]]
 if os.environ.get("HP_TRACE"):  # one more launch, traced on SM 0
     f(buf, 1)
     pkg.chain_hash_batch(tokens, tok_off, 16, key_off=key_off, keys=keys)
@@ -55,7 +55,7 @@ if os.environ.get("HP_TRACE"):  # one more launch, traced on SM 0
     print(f"trace: {n_ev} events -> {out}")
 W = int(os.environ.get("KVX_HASH_FOLD_CTA_WARPS", "28"))
 share = int(os.environ.get("KVX_HASH_FOLD_SHARE", "1"))
-P = sum(1 for w in range(W - 1) if w % 4 != (W - 1) % 4 or w // 4 < share)
+P = sum(1 for w in range(W - 2) if w % 4 != (W - 1) % 4 or w // 4 < share)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 us = e0.elapsed_time(e1) / runs * 1e3
 prod = v[0:5]
@@ -67,5 +67,6 @@ print("producer cycles per warp per launch: " + ", ".join(
 fold = v[5] + v[6]
 print(f"folder cycles per launch: idle {v[5] / runs / sms:.0f} ({v[5] / max(fold, 1):.1%}), "
       f"windows {v[6] / runs / sms:.0f}; iterations per SM {v[7] / runs / sms:.1f}")
-print(f"claim attempts per SM per launch: none eligible {v[10] / runs / sms:.0f}, "
-      f"picked {v[11] / runs / sms:.0f} (tasks ~{sum(1 for _ in [0]) and 0})")
+print(f"dispatcher per SM per launch: full-ring stalls {v[10] / runs / sms:.0f}, "
+      f"tasks {v[11] / runs / sms:.0f}; idle {v[12] / runs / sms:.0f} cycles, "
+      f"filling {v[13] / runs / sms:.0f} cycles")
