@@ -1145,17 +1145,55 @@ def bench_match_sharded(args, dev, rank, world, s, o):
         step(timed=True)
     e1.record(s)
     s.synchronize()
-    ms = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
+    ms_sep = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
     hs = th.summary()
     lens = np.diff(mw.tok_off)
     longest = int((lens.max() + mw.block_size - 1) // mw.block_size)
+
+    # the same step with the exchange inside the kernels (kvx_xmatch_hash_match):
+    # the hash stores every key into every GPU's key buffer as it is produced and
+    # each GPU's match kernel follows the whole batch beside its hash
+    def step_fused():
+        return xm.hash_match(B.tokens, B.tok_off, r0, r1, mw.block_size, B.key_off, [idx],
+                             [rank], out=(best_len, best_id), stream=s)
+
+    ms_fused = None
+    fused_note = None
+    try:
+        for _ in range(args.warmup):
+            step_fused()
+        s.synchronize()
+    except pkg.kvx.ValidationError as exc:  # a peer shares this GPU: separate steps only
+        fused_note = str(exc)
+    if fused_note is None:
+        dist.barrier()
+        e0.record(s)
+        for _ in range(args.steps):
+            _, _, fkeys = step_fused()
+        e1.record(s)
+        s.synchronize()
+        ms_fused = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
+        pkg.kvx.check(pkg.kvx._L.kvx_hash_match_check(pkg.kvx._stream(s)))
+        ok = (np.array_equal(fkeys.cpu().numpy()[: B.n_blocks], k_ref)
+              and np.array_equal(best_len.cpu().numpy(), want_len)
+              and np.array_equal(best_id.cpu().numpy(), want_id))
+        if not ok:
+            raise SystemExit("FUSED SHARDED STAGE-1 PARITY FAILURE (keys or best match)")
+    ms = ms_fused if ms_fused is not None else ms_sep
     out = {"value": B.n_blocks / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms,
            "scaling": "strong",
+           "step": ("kvx_xmatch_hash_match: each GPU hashes its shard and stores every key "
+                    "into every GPU's key buffer from the hash kernel (NVLink stores); each "
+                    "GPU's match kernel follows the whole batch beside its hash and MAXes "
+                    "results into every GPU (remote atomics); stream-memop flags, no "
+                    "collective" if ms_fused is not None else
+                    "hash shard, kvx_xmatch_share_keys (copy engine), kvx_xmatch_run"),
+           "ms_per_step_separate": ms_sep,
+           "fused_unavailable": fused_note,
            "hash_shard_ms_max": max_over_ranks(hs["avg_ms"], d),
            "layout": f"one 4096-request batch; requests sharded over {world} GPUs by tokens "
-                     "for hashing; keys pushed to every GPU by the copy engine "
-                     "(kvx_xmatch_share_keys); each GPU one prefill instance, global best "
-                     "combined in the match kernel (kvx_xmatch_run)",
+                     "for hashing; each GPU one prefill instance, global best combined in "
+                     "the match kernel",
            "longest_request_blocks": longest,
            "note": "a request's block keys are one sequential chain_hash chain, so the "
                    "longest request bounds the sharded hash (~1,536 dependent steps)",

@@ -1064,9 +1064,12 @@ namespace kvx {
 int match_follow_launch(const kvx_index* const* idx, const int32_t* inst_ids, int64_t n_inst,
                         const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
                         int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
-                        const int32_t* d_order, unsigned long long* d_claim, void* stream) {
+                        const int32_t* d_order, unsigned long long* d_claim, void* stream,
+                        uint64_t* const* dests, int n_dests) {
   MatchParams p{};
   p.n_inst = static_cast<int32_t>(n_inst);
+  p.n_dests = n_dests;  // cross-GPU: packed atomicMax into every rank's result buffer
+  for (int j = 0; j < n_dests; ++j) p.dests[j] = reinterpret_cast<unsigned long long*>(dests[j]);
   const int dev = idx[0]->device;
   for (int64_t i = 0; i < n_inst; ++i) {
     KVX_REQUIRE(idx[i] != nullptr && idx[i]->device == dev,
@@ -1138,14 +1141,20 @@ extern "C" int kvx_hash_match_check(void* stream) {
 struct kvx_xmatch {
   int device = 0, rank = 0, world = 1;
   int64_t max_req = 0;
-  uint8_t* mem = nullptr;  // [buf0 | buf1 | flags[KVX_MAX_PEERS] | keyflags[KVX_MAX_PEERS]]
+  // [buf0 | buf1 | flags | keyflags | readyflags | doneflags], KVX_MAX_PEERS words per flag set
+  uint8_t* mem = nullptr;
   uint64_t* peer_buf[KVX_MAX_PEERS][2] = {};
   uint64_t* peer_flags[KVX_MAX_PEERS] = {};
   void* peer_mem[KVX_MAX_PEERS] = {};
   uint64_t epoch = 0;
-  // shared key buffer (optional)
+  // shared key buffer (optional): two halves, by the parity of the fused step
   int64_t max_keys = 0;
   int64_t* keys = nullptr;
+  uint64_t fused_epoch = 0;
+  bool peer_same_gpu = false;  // some peer shares this physical GPU: no fused stage 1
+  int32_t* order = nullptr;    // fused stage 1: whole-batch longest-first order + claim counter
+  unsigned long long* claim = nullptr;
+  uint8_t uuid[16] = {};
   int64_t* peer_keys[KVX_MAX_PEERS] = {};
   uint64_t key_epoch = 0;
   cudaStream_t copy_stream = nullptr;
@@ -1153,10 +1162,17 @@ struct kvx_xmatch {
   uint64_t* buf(int b) const { return reinterpret_cast<uint64_t*>(mem) + b * max_req; }
   uint64_t* flags() const { return reinterpret_cast<uint64_t*>(mem) + 2 * max_req; }
   uint64_t* keyflags() const { return flags() + KVX_MAX_PEERS; }
+  uint64_t* readyflags() const { return flags() + 2 * KVX_MAX_PEERS; }
+  uint64_t* doneflags() const { return flags() + 3 * KVX_MAX_PEERS; }
   size_t bytes() const {
-    return (2 * static_cast<size_t>(max_req) + 2 * KVX_MAX_PEERS) * sizeof(uint64_t);
+    return (2 * static_cast<size_t>(max_req) + 4 * KVX_MAX_PEERS) * sizeof(uint64_t);
   }
 };
+
+extern "C" {
+static int xmatch_finish(kvx_xmatch* x, uint64_t e, int64_t n_req, int64_t* d_best_len,
+                         int32_t* d_best_id, cudaStream_t s);
+}
 
 namespace {
 struct XmatchBlob {
@@ -1165,6 +1181,7 @@ struct XmatchBlob {
   uint8_t handle[KVX_IPC_HANDLE_BYTES];
   int64_t max_keys;  // 0: no shared key buffer
   uint8_t key_handle[KVX_IPC_HANDLE_BYTES];
+  uint8_t uuid[16];  // physical GPU
 };
 constexpr int32_t kXmatchMagic = 0x6b76786d;  // "kvxm"
 }  // namespace
@@ -1192,6 +1209,9 @@ int kvx_xmatch_create(int device, int rank, int world, int64_t max_req, kvx_xmat
   x->peer_buf[rank][0] = x->buf(0);
   x->peer_buf[rank][1] = x->buf(1);
   x->peer_flags[rank] = x->flags();
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, device) == cudaSuccess)
+    std::memcpy(x->uuid, &prop.uuid, sizeof(x->uuid));
   *out = x;
   return KVX_OK;
 }
@@ -1207,6 +1227,8 @@ int kvx_xmatch_destroy(kvx_xmatch* x) {
   if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
   if (x->copy_dep) cudaEventDestroy(x->copy_dep);
   if (x->keys) cudaFree(x->keys);
+  if (x->order) cudaFree(x->order);
+  if (x->claim) cudaFree(x->claim);
   if (x->mem) cudaFree(x->mem);
   delete x;
   return KVX_OK;
@@ -1225,6 +1247,7 @@ int kvx_xmatch_export(kvx_xmatch* x, uint8_t* blob, int64_t cap, int64_t* len) {
   int rc = kvx_ipc_export(x->mem, b.handle);
   if (rc) return rc;
   b.max_keys = x->max_keys;
+  std::memcpy(b.uuid, x->uuid, sizeof(b.uuid));
   if (x->keys) {
     rc = kvx_ipc_export(x->keys, b.key_handle);
     if (rc) return rc;
@@ -1243,6 +1266,7 @@ int kvx_xmatch_connect(kvx_xmatch* x, const uint8_t* blob, int64_t len) {
               "kvx_xmatch_connect: peer does not match (rank / world / max_req / key buffer)");
   if (b.rank == x->rank) return KVX_OK;  // self
   KVX_REQUIRE(x->peer_mem[b.rank] == nullptr, "kvx_xmatch_connect: peer already connected");
+  if (std::memcmp(b.uuid, x->uuid, sizeof(b.uuid)) == 0) x->peer_same_gpu = true;
   void* p = nullptr;
   int rc = kvx_ipc_open(b.handle, x->device, &p);
   if (rc) return rc;
@@ -1270,7 +1294,7 @@ int kvx_xmatch_key_buffer(kvx_xmatch* x, int64_t max_keys, int64_t** d_keys) {
     KVX_REQUIRE(j == x->rank || x->peer_mem[j] == nullptr,
                 "kvx_xmatch_key_buffer: call before exporting / connecting");
   DeviceGuard g(x->device);
-  KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&x->keys), sizeof(int64_t) * max_keys));
+  KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&x->keys), 2 * sizeof(int64_t) * max_keys));
   KVX_CUDA(cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking));
   KVX_CUDA(cudaEventCreateWithFlags(&x->copy_dep, cudaEventDisableTiming));
   x->max_keys = max_keys;
@@ -1332,6 +1356,14 @@ int kvx_xmatch_run(kvx_xmatch* x, const kvx_index* const* idx, const int32_t* in
                         true, stream, dests, x->world);
     if (rc) return rc;
   }
+  return xmatch_finish(x, e, n_req, d_best_len, d_best_id, s);
+}
+
+// After every rank's match atomics for step e: announce, wait for all, unpack.
+static int xmatch_finish(kvx_xmatch* x, uint64_t e, int64_t n_req, int64_t* d_best_len,
+                         int32_t* d_best_id, cudaStream_t s) {
+  const int b = static_cast<int>(e & 1);
+  void* stream = s;
   // the other parity's buffer was unpacked last step: zero it before announcing
   KVX_CUDA(cudaMemsetAsync(x->buf(b ^ 1), 0, sizeof(uint64_t) * x->max_req, s));
   for (int j = 0; j < x->world; ++j) {  // "my atomics for step e have landed" -> every rank
@@ -1347,6 +1379,110 @@ int kvx_xmatch_run(kvx_xmatch* x, const kvx_index* const* idx, const int32_t* in
         reinterpret_cast<const unsigned long long*>(x->buf(b)), d_best_len, d_best_id, n_req);
     KVX_LAUNCH_CHECK("unpack_best_kernel");
   }
+  return KVX_OK;
+}
+
+
+// Request-sharded stage 1 with the exchange inside the kernels (see kvx.h).
+// Per step e (parity par = e & 1 selects the key-buffer half):
+//   wait ready(e) from every peer      (their half `par` is preset to -1)
+//   hash this rank's shard -> keys into the local half AND every peer's half
+//   follow: match the WHOLE batch against the local instances as keys land
+//           (local or NVLink-stored), packed atomicMax into every rank's result
+//   signal done(e) to every peer        (my stores into their half `par` ended)
+//   announce / wait / unpack the results (xmatch_finish)
+//   wait done(e - 1) from every peer, preset half par ^ 1, signal ready(e + 1)
+// Every wait is a stream memop; nothing blocks the host.
+int kvx_xmatch_hash_match(kvx_xmatch* x, const int32_t* d_tokens, const int64_t* d_tok_off,
+                          int64_t r0, int64_t r1, int64_t bs, const int64_t* d_key_off,
+                          int64_t n_req, const kvx_index* const* idx, const int32_t* inst_ids,
+                          int64_t n_inst, int64_t* d_best_len, int32_t* d_best_id,
+                          int64_t** d_keys_out, void* stream) {
+  KVX_REQUIRE(x && x->keys, "kvx_xmatch_hash_match: no key buffer");
+  KVX_REQUIRE(n_inst >= 1, "find_best_prefix_match: empty prefill pool");
+  KVX_REQUIRE(n_inst <= KVX_MAX_INSTANCES, "kvx_xmatch_hash_match: too many instances");
+  KVX_REQUIRE(idx != nullptr && inst_ids != nullptr, "kvx_xmatch_hash_match: NULL instances");
+  KVX_REQUIRE(n_req >= 1 && n_req <= x->max_req, "kvx_xmatch_hash_match: n_req out of range");
+  KVX_REQUIRE(0 <= r0 && r0 <= r1 && r1 <= n_req, "kvx_xmatch_hash_match: bad shard");
+  KVX_REQUIRE(d_tokens && d_tok_off && d_key_off && d_best_len && d_best_id,
+              "kvx_xmatch_hash_match: NULL array");
+  KVX_REQUIRE(bs >= 16 && bs % 16 == 0 && (reinterpret_cast<uintptr_t>(d_tokens) & 15) == 0,
+              "kvx_xmatch_hash_match: needs bs % 16 == 0 and 16-byte aligned tokens");
+  KVX_REQUIRE(!x->peer_same_gpu,
+              "kvx_xmatch_hash_match: a peer shares this GPU (its kernels would wait on ours); "
+              "use kvx_xmatch_share_keys + kvx_xmatch_run");
+  for (int j = 0; j < x->world; ++j)
+    KVX_REQUIRE(x->peer_keys[j] != nullptr && x->peer_buf[j][0] != nullptr,
+                "kvx_xmatch_hash_match: not connected to every rank");
+  DeviceGuard g(x->device);
+  cudaStream_t s = as_stream(stream);
+  if (!x->order) {
+    KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&x->order), sizeof(int32_t) * x->max_req));
+    KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&x->claim), 64));
+  }
+  const uint64_t e = ++x->fused_epoch;
+  const int par = static_cast<int>(e & 1);
+  int64_t* mine = x->keys + par * x->max_keys;
+  int rc = KVX_OK;
+  // a half is preset whole (all bytes 0xff: every key -1), so the next step
+  // may be a batch of any size
+  const size_t half_bytes = sizeof(int64_t) * static_cast<size_t>(x->max_keys);
+  if (e == 1) {  // the first step's half: preset and announce
+    KVX_CUDA(cudaMemsetAsync(mine, 0xff, half_bytes, s));
+    for (int j = 0; j < x->world; ++j) {
+      if (j == x->rank) continue;
+      rc = kvx_signal_write(stream, x->peer_flags[j] + 2 * KVX_MAX_PEERS + x->rank, e);
+      if (rc) return rc;
+    }
+  }
+  for (int j = 0; j < x->world; ++j) {  // every peer's half `par` is preset
+    if (j == x->rank) continue;
+    rc = kvx_signal_wait(stream, x->readyflags() + j, e);
+    if (rc) return rc;
+  }
+  // whole-batch longest-first order for the follower (also zeroes its claim counter)
+  rc = order_by_length(d_key_off, n_req, x->order, x->claim, s);
+  if (rc) return rc;
+  int64_t* peers[KVX_MAX_PEERS];
+  int n_peer = 0;
+  for (int k = 1; k < x->world; ++k) {  // start with the next rank: spread the stores
+    const int j = (x->rank + k) % x->world;
+    peers[n_peer++] = x->peer_keys[j] + par * x->max_keys;
+  }
+  if (r1 > r0) {
+    bool published = false;
+    rc = hash_publish_launch(d_tokens, d_tok_off + r0, r1 - r0, bs, d_key_off + r0, mine, peers,
+                             n_peer, stream, &published);
+    if (rc) return rc;
+    KVX_REQUIRE(published, "kvx_xmatch_hash_match: the publishing hash kernel did not run");
+  }
+  const uint64_t me = ++x->epoch;  // the result exchange's own step counter
+  const int b = static_cast<int>(me & 1);
+  uint64_t* dests[KVX_MAX_PEERS];
+  for (int j = 0; j < x->world; ++j) dests[j] = x->peer_buf[j][b];
+  rc = match_follow_launch(idx, inst_ids, n_inst, mine, d_key_off, n_req, nullptr, nullptr,
+                           nullptr, x->order, x->claim, stream, dests, x->world);
+  if (rc) return rc;
+  for (int j = 0; j < x->world; ++j) {  // my stores into every peer's half `par` are done
+    if (j == x->rank) continue;
+    rc = kvx_signal_write(stream, x->peer_flags[j] + 3 * KVX_MAX_PEERS + x->rank, e);
+    if (rc) return rc;
+  }
+  rc = xmatch_finish(x, me, n_req, d_best_len, d_best_id, s);
+  if (rc) return rc;
+  // next step's half: every peer finished storing into it (step e - 1), then preset
+  for (int j = 0; j < x->world; ++j) {
+    if (j == x->rank) continue;
+    rc = kvx_signal_wait(stream, x->doneflags() + j, e - 1);
+    if (rc) return rc;
+  }
+  KVX_CUDA(cudaMemsetAsync(x->keys + (par ^ 1) * x->max_keys, 0xff, half_bytes, s));
+  for (int j = 0; j < x->world; ++j) {
+    if (j == x->rank) continue;
+    rc = kvx_signal_write(stream, x->peer_flags[j] + 2 * KVX_MAX_PEERS + x->rank, e + 1);
+    if (rc) return rc;
+  }
+  if (d_keys_out) *d_keys_out = mine;
   return KVX_OK;
 }
 

@@ -95,6 +95,8 @@ _sig("kvx_hash_match_batch", C.c_int, _vp, _vp, _i64, _i64, _vp, _vp, C.POINTER(
 _sig("kvx_hash_match_check", C.c_int, _vp)
 _sig("kvx_xmatch_key_buffer", C.c_int, _vp, _i64, C.POINTER(_vp))
 _sig("kvx_xmatch_share_keys", C.c_int, _vp, _i64, _i64, _vp)
+_sig("kvx_xmatch_hash_match", C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64,
+     C.POINTER(_vp), C.POINTER(_i32), _i64, _vp, _vp, C.POINTER(_vp), _vp)
 _sig("kvx_index_create", C.c_int, C.c_int, _i64, C.POINTER(_vp))
 _sig("kvx_index_destroy", C.c_int, _vp)
 _sig("kvx_index_device", C.c_int, _vp)
@@ -429,6 +431,7 @@ class XMatch:
         hashing); call before export()."""
         p = _vp()
         check(_L.kvx_xmatch_key_buffer(self.h, max_keys, C.byref(p)))
+        self.max_keys = max_keys
         # valid while this XMatch lives (no back reference: no cycle)
         return _wrap_device_bytes(int(p.value), 8 * max_keys, self.device).view(torch.int64)
 
@@ -436,6 +439,36 @@ class XMatch:
         """Push this rank's hashed shard [key_lo, key_hi) to every peer (copy
         engine over NVLink); `stream` then waits for every peer's shard."""
         check(_L.kvx_xmatch_share_keys(self.h, key_lo, key_hi, _stream(stream)))
+
+    def hash_match(self, tokens: torch.Tensor, tok_off: torch.Tensor, r0: int, r1: int, bs: int,
+                   key_off: torch.Tensor, indices: Sequence[BlockIndex], inst_ids: Sequence[int],
+                   out=None, stream=None):
+        """Request-sharded stage 1 with the exchange inside the kernels: this
+        rank hashes requests [r0, r1) of the batch and stores every key into
+        every rank's key buffer as it is produced; each rank's match kernel
+        follows the keys of the WHOLE batch against its instances and MAXes
+        the result into every rank's buffer.  Collective, once per step.
+        Needs key_buffer() sized for the batch, bs % 16 == 0 and one GPU per
+        rank.  Returns (best_len, best_id, keys) -- keys: this step's batch
+        keys on this rank (valid until the step after next)."""
+        n_inst = len(indices)
+        n_req = len(key_off) - 1
+        arr = (_vp * max(n_inst, 1))(*[i.h for i in indices])
+        ids = (_i32 * max(n_inst, 1))(*[int(i) for i in inst_ids])
+        if out is None:
+            out = (torch.empty(n_req, dtype=torch.int64, device=key_off.device),
+                   torch.empty(n_req, dtype=torch.int32, device=key_off.device))
+        best_len, best_id = out
+        n_keys = int(key_off[-1].item())
+        if n_keys > getattr(self, "max_keys", 0):
+            raise ValidationError("XMatch.hash_match: the batch has more keys than key_buffer()")
+        kp = _vp()
+        check(_L.kvx_xmatch_hash_match(self.h, _ptr(tokens), _ptr(tok_off), r0, r1, bs,
+                                       _ptr(key_off), n_req, arr, ids, n_inst, _ptr(best_len),
+                                       _ptr(best_id), C.byref(kp), _stream(stream)))
+        keys = (_wrap_device_bytes(int(kp.value), 8 * n_keys, self.device).view(torch.int64)
+                if kp.value and n_keys else None)
+        return best_len, best_id, keys
 
     def run(self, indices: Sequence[BlockIndex], inst_ids: Sequence[int], keys: torch.Tensor,
             key_off: torch.Tensor, out=None, stream=None):

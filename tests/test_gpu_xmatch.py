@@ -32,6 +32,29 @@ def test_xmatch_shared_gpu_bit_exact(kvx):
     assert r.returncode == 0 and "XMATCH OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_xmatch_fused_stage1_two_gpus():
+    """Request-sharded hash with the keys stored into every GPU's buffer from
+    the hash kernel, and each GPU's match kernel following them."""
+    n = min(torch.cuda.device_count(), 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29557",
+           "tests/xmatch_stage1_worker.py"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "XMATCH STAGE1 OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_xmatch_fused_stage1_refuses_shared_gpu(kvx):
+    """Two processes on one GPU: the fused call must refuse (its match kernel
+    would wait on the other process's hash kernel on the same GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29567",
+           "tests/xmatch_stage1_worker.py"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "KVX_SHARE_GPU": "1"})
+    assert r.returncode == 0 and "XMATCH STAGE1 OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_xmatch_validation(kvx):
     with pytest.raises(kvx.ValidationError):
         kvx.XMatch(0, 2, 2, 16)  # rank out of range
