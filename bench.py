@@ -1153,8 +1153,10 @@ def bench_match_sharded(args, dev, rank, world, s, o):
     # the same step with the exchange inside the kernels (kvx_xmatch_hash_match):
     # the hash stores every key into every GPU's key buffer as it is produced and
     # each GPU's match kernel follows the whole batch beside its hash
+    bounds = [0] + [b for _, b in shard_by_tokens(mw.tok_off, world)]
+
     def step_fused():
-        return xm.hash_match(B.tokens, B.tok_off, r0, r1, mw.block_size, B.key_off, [idx],
+        return xm.hash_match(B.tokens, B.tok_off, bounds, mw.block_size, B.key_off, [idx],
                              [rank], out=(best_len, best_id), stream=s)
 
     ms_fused = None
@@ -1174,7 +1176,7 @@ def bench_match_sharded(args, dev, rank, world, s, o):
         s.synchronize()
         ms_fused = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
         pkg.kvx.check(pkg.kvx._L.kvx_hash_match_check(pkg.kvx._stream(s)))
-        ok = (np.array_equal(fkeys.cpu().numpy()[: B.n_blocks], k_ref)
+        ok = (np.array_equal(fkeys.cpu().numpy()[k0:k1], k_ref[k0:k1])  # this GPU's shard
               and np.array_equal(best_len.cpu().numpy(), want_len)
               and np.array_equal(best_id.cpu().numpy(), want_id))
         if not ok:
@@ -1182,11 +1184,11 @@ def bench_match_sharded(args, dev, rank, world, s, o):
     ms = ms_fused if ms_fused is not None else ms_sep
     out = {"value": B.n_blocks / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms,
            "scaling": "strong",
-           "step": ("kvx_xmatch_hash_match: each GPU hashes its shard and stores every key "
-                    "into every GPU's key buffer from the hash kernel (NVLink stores); each "
-                    "GPU's match kernel follows the whole batch beside its hash and MAXes "
-                    "results into every GPU (remote atomics); stream-memop flags, no "
-                    "collective" if ms_fused is not None else
+           "step": ("kvx_xmatch_hash_match: each GPU hashes its shard into its own key "
+                    "buffer; each GPU's match kernel runs beside its hash and follows the "
+                    "whole batch's keys where they are produced (NVLink loads of the owner's "
+                    "buffer), MAXing results into every GPU (remote atomics); stream-memop "
+                    "flags, no collective" if ms_fused is not None else
                     "hash shard, kvx_xmatch_share_keys (copy engine), kvx_xmatch_run"),
            "ms_per_step_separate": ms_sep,
            "fused_unavailable": fused_note,

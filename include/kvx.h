@@ -200,21 +200,23 @@ int kvx_xmatch_run(kvx_xmatch* x, const kvx_index* const* idx, const int32_t* in
  * stream.  Collective: every rank calls share_keys then run once per step. */
 int kvx_xmatch_key_buffer(kvx_xmatch* x, int64_t max_keys, int64_t** d_keys);
 int kvx_xmatch_share_keys(kvx_xmatch* x, int64_t key_lo, int64_t key_hi, void* stream);
-/* Request-sharded stage 1 with the exchange inside the kernels (replaces
- * chain_hash_batch + share_keys + run when every rank has its own GPU): this
- * rank hashes requests [r0, r1) of the batch (d_tok_off / d_key_off: the
- * WHOLE batch's offsets, n_req + 1 each) and its hash kernel stores every key
- * into every rank's key buffer (NVLink stores) as it is produced; every rank's
- * match kernel runs beside its hash and follows the keys of the whole batch
- * (keys are preset to -1 and polled) against its instances, MAXing each
- * request's packed best into every rank's result buffer.  Stream-ordered
- * flags order the steps (two key-buffer halves by step parity); the host
- * never blocks.  Collective, once per step, same n_req and bs on every rank.
- * Needs kvx_xmatch_key_buffer (>= the batch's keys), bs % 16 == 0, 16-byte
- * aligned tokens; returns KVX_EINVAL if a peer shares this GPU (its kernels
- * would wait on ours).  *d_keys_out (may be NULL): this step's key buffer. */
+/* Request-sharded stage 1 with the key exchange inside the match kernel
+ * (replaces chain_hash_batch + share_keys + run when every rank has its own
+ * GPU): rank k hashes requests [shard_bounds[k], shard_bounds[k+1]) of the
+ * batch (shard_bounds: host array of world + 1, from 0 to n_req, the same on
+ * every rank; d_tok_off / d_key_off: the WHOLE batch's offsets) into its own
+ * key buffer, and every rank's match kernel runs beside its hash and follows
+ * the keys of the whole batch where they are produced -- local, or NVLink
+ * loads of the owning peer's buffer (keys are preset to -1 and polled) --
+ * against its instances, MAXing each request's packed best into every rank's
+ * result buffer.  Stream-ordered flags order the steps (two key-buffer halves
+ * by step parity); the host never blocks.  Collective, once per step, same
+ * n_req, bs and bounds on every rank.  Needs kvx_xmatch_key_buffer (>= the
+ * batch's keys), bs % 16 == 0, 16-byte aligned tokens; KVX_EINVAL if a peer
+ * shares this GPU (its kernels would wait on ours).  *d_keys_out (may be
+ * NULL): this rank's key buffer of the step (its own shard's keys). */
 int kvx_xmatch_hash_match(kvx_xmatch* x, const int32_t* d_tokens, const int64_t* d_tok_off,
-                          int64_t r0, int64_t r1, int64_t bs, const int64_t* d_key_off,
+                          const int64_t* shard_bounds, int64_t bs, const int64_t* d_key_off,
                           int64_t n_req, const kvx_index* const* idx, const int32_t* inst_ids,
                           int64_t n_inst, int64_t* d_best_len, int32_t* d_best_id,
                           int64_t** d_keys_out, void* stream);

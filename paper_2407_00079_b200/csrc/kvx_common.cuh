@@ -91,13 +91,15 @@ int match_follow_launch(const kvx_index* const* idx, const int32_t* inst_ids, in
                         const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
                         int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
                         const int32_t* d_order, unsigned long long* d_claim, void* stream,
-                        uint64_t* const* dests = nullptr, int n_dests = 0);
+                        uint64_t* const* dests = nullptr, int n_dests = 0,
+                        const int64_t* const* owner_keys = nullptr,
+                        const int64_t* owner_end = nullptr, int n_owner = 0);
 // Requests of a batch in decreasing block count (kvx_hash.cu).
 int order_by_length(const int64_t* d_key_off, int64_t n_req, int32_t* d_order,
                     unsigned long long* d_ws, cudaStream_t s);
 int hash_publish_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req,
-                        int64_t bs, const int64_t* d_key_off, int64_t* d_keys,
-                        int64_t* const* peers, int n_peer, void* stream, bool* published);
+                        int64_t bs, const int64_t* d_key_off, int64_t* d_keys, void* stream,
+                        bool* published);
 
 }  // namespace kvx
 

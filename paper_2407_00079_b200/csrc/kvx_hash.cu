@@ -346,15 +346,9 @@ struct alignas(16) SubDesc {
 // preset to -1 (no key is negative: chain_hash masks the sign bit), and a
 // match kernel beside the hash reads each key once it is no longer -1.  No
 // fence or extra store on the hash's side (a release per round would wait for
-// the round's in-flight token prefetches).  With peers (request-sharded
-// stage 1 over several GPUs, kvx_xmatch_hash_match) the folding lane also
-// stores every key into each peer GPU's copy of the batch key buffer (same
-// offsets; CUDA IPC mappings, NVLink stores), where that GPU's match kernel
-// follows it the same way.
+// the round's in-flight token prefetches).
 struct Publish {
   int enabled;
-  int n_peer;
-  int64_t* peer[KVX_MAX_PEERS];
 };
 
 // Staging of one request stream (one chain per lane) of one half-warp.
@@ -814,12 +808,12 @@ __device__ __forceinline__ Ctl make_ctl(HalfSmem& H, const uint32_t* zero, int s
   return c;
 }
 
-template <bool kLazyIssue, bool kPeers>
+template <bool kLazyIssue>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
     const int32_t* __restrict__ tokens, const int64_t* __restrict__ tok_off, int64_t n_req,
     int bs, const int64_t* __restrict__ key_off, int64_t* __restrict__ keys,
-    const int32_t* __restrict__ order, unsigned long long* ctr, int prio,
-    const __grid_constant__ Publish pubv) {
+    const int32_t* __restrict__ order, unsigned long long* ctr, int prio, Publish pubv) {
+  (void)pubv;
   extern __shared__ __align__(16) unsigned char hw_smem_raw[];
   WarpSmem<1>& S = reinterpret_cast<WarpSmem<1>*>(hw_smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -886,11 +880,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
         const uint64_t in = (static_cast<uint64_t>(c.hi[s]) << 32) | c.lo[s];
         h = chain_hash(h, in);
         if (s == kContentLanes - 1) h14 = h;
-        if (s < kContentLanes && folder && fn > 0) {
-          keys[fkb + s] = h;
-          if (kPeers)
-            for (int q = 0; q < pubv.n_peer; ++q) pubv.peer[q][fkb + s] = h;
-        }
+        if (s < kContentLanes && folder && fn > 0) keys[fkb + s] = h;
       }
       if (folder) h = fn > 0 ? h14 : h0;
       // next sub-round's work, scheduled into the chain's idle issue slots
@@ -906,11 +896,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) halfwarp_hash_kernel_p(
         const int64_t hn = chain_hash(h, in);
         const bool act = s < c.lim;
         h = act ? hn : h;
-        if (folder && fn > 0 && act) {
-          keys[fkb + s] = h;
-          if (kPeers)
-            for (int q = 0; q < pubv.n_peer; ++q) pubv.peer[q][fkb + s] = h;
-        }
+        if (folder && fn > 0 && act) keys[fkb + s] = h;
       }
       if (kLazyIssue) issue_p(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
       else issue_p0(P, H, static_cast<int>((it + kPrefetch) % kSlots), hl, j, bs, nsub, tokens);
@@ -1067,7 +1053,7 @@ extern "C" int kvx_chain_hash_batch(const int32_t* d_tokens, const int64_t* d_to
                                     int64_t* d_keys, void* stream) {
   bool published = false;
   return hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream,
-                     hw::Publish{}, &published);
+                     hw::Publish{0}, &published);
 }
 
 namespace {
@@ -1132,13 +1118,10 @@ int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req
       KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel<1, true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hw::kMaxCtaSmem)));
-      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p<true, false>,
+      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p<true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hw::kMaxCtaSmem)));
-      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p<false, false>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(hw::kMaxCtaSmem)));
-      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p<true, true>,
+      KVX_CUDA(cudaFuncSetAttribute(hw::halfwarp_hash_kernel_p<false>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(hw::kMaxCtaSmem)));
       W.hw_attr[dev] = true;
@@ -1182,11 +1165,10 @@ int hash_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req
       const char* e = std::getenv("KVX_HASH_ISSUE");  // 0: per-chunk sizes every sub-round
       return !(e && e[0] == '0');
     }();
-    if (pipelined || pub.n_peer > 0) {
+    if (pipelined) {
       KVX_CUDA(cudaLaunchKernelEx(&cfg,
-                                  pub.n_peer > 0 ? hw::halfwarp_hash_kernel_p<true, true>
-                                  : lazy_issue   ? hw::halfwarp_hash_kernel_p<true, false>
-                                                 : hw::halfwarp_hash_kernel_p<false, false>,
+                                  lazy_issue ? hw::halfwarp_hash_kernel_p<true>
+                                             : hw::halfwarp_hash_kernel_p<false>,
                                   d_tokens, d_tok_off, n_req, bsi, d_key_off, d_keys,
                                   static_cast<const int32_t*>(order), ctr, order ? prio : 0, pub));
       *published = pub.enabled != 0;
@@ -1269,10 +1251,8 @@ extern "C" int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_to
     KVX_CUDA(cudaMemsetAsync(d_best_len, 0, sizeof(int64_t) * n_req, s));
   bool published = false;
   const int32_t* order = nullptr;
-  hw::Publish pub1{};
-  pub1.enabled = 1;
   int rc = hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream,
-                       pub1, &published, &order);
+                       hw::Publish{1}, &published, &order);
   if (rc) return rc;
   if (!published)  // the producer / fold kernel (bs % 16 != 0): hash, then match
     return kvx_match_prefix_batch(idx, inst_ids, n_inst, d_keys, d_key_off, n_req, d_len_out,
@@ -1287,19 +1267,14 @@ extern "C" int kvx_hash_match_batch(const int32_t* d_tokens, const int64_t* d_to
 }
 
 namespace kvx {
-// Request-sharded stage 1 (kvx_xmatch_hash_match): this rank's shard hashed
-// with every key also stored into the peers' copies of the batch key buffer.
-// *published: the half-warp kernel ran (bs % 16 == 0, 16-byte aligned tokens);
-// otherwise the keys are local only.
+// The hash of kvx_hash_match_batch (keys preset to -1 by the caller; a match
+// kernel may follow them) for other callers: request-sharded stage 1
+// (kvx_xmatch_hash_match).  *published: the half-warp kernel ran (bs % 16 ==
+// 0, 16-byte aligned tokens); otherwise a kernel that cannot be followed ran.
 int hash_publish_launch(const int32_t* d_tokens, const int64_t* d_tok_off, int64_t n_req,
-                        int64_t bs, const int64_t* d_key_off, int64_t* d_keys,
-                        int64_t* const* peers, int n_peer, void* stream, bool* published) {
-  KVX_REQUIRE(n_peer >= 0 && n_peer < KVX_MAX_PEERS, "hash_publish_launch: too many peers");
-  hw::Publish pub{};
-  pub.enabled = 1;
-  pub.n_peer = n_peer;
-  for (int j = 0; j < n_peer; ++j) pub.peer[j] = peers[j];
-  return ::hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream, pub, published);
+                        int64_t bs, const int64_t* d_key_off, int64_t* d_keys, void* stream,
+                        bool* published) {
+  return ::hash_launch(d_tokens, d_tok_off, n_req, bs, d_key_off, d_keys, stream, hw::Publish{1},
+                       published);
 }
-
 }  // namespace kvx

@@ -239,6 +239,11 @@ struct MatchParams {
   // every rank's result buffer (peer mappings; NVLink remote atomics)
   unsigned long long* dests[KVX_MAX_PEERS];
   int32_t n_dests;
+  // request-sharded batches (follower only): the keys of requests
+  // [owner_end[j-1], owner_end[j]) live in owner_keys[j] (a peer GPU's buffer)
+  const int64_t* owner_keys[KVX_MAX_PEERS];
+  int64_t owner_end[KVX_MAX_PEERS];
+  int32_t n_owner;
 };
 
 // U independent probe chains per lane: every chain's next slot load is issued
@@ -544,7 +549,13 @@ __global__ void __launch_bounds__(G * 32) match_follow_kernel(
     if (r < 0) return;
     const int64_t base = key_off[r];
     const int64_t n = key_off[r + 1] - base;
-    const int64_t* q = keys + base;
+    const int64_t* kb = keys;
+    if (p.n_owner > 0) {  // read the keys where their shard's GPU stores them (NVLink loads)
+      int j = 0;
+      while (j + 1 < p.n_owner && r >= p.owner_end[j]) ++j;
+      kb = p.owner_keys[j];
+    }
+    const int64_t* q = kb + base;
     for (int i = 0; i < p.n_inst; ++i) {
       const int64_t t = r * p.n_inst + i;
       const int64_t* __restrict__ tk = p.keys[i];
@@ -1065,8 +1076,14 @@ int match_follow_launch(const kvx_index* const* idx, const int32_t* inst_ids, in
                         const int64_t* d_keys, const int64_t* d_key_off, int64_t n_req,
                         int64_t* d_len_out, int64_t* d_best_len, int32_t* d_best_id,
                         const int32_t* d_order, unsigned long long* d_claim, void* stream,
-                        uint64_t* const* dests, int n_dests) {
+                        uint64_t* const* dests, int n_dests, const int64_t* const* owner_keys,
+                        const int64_t* owner_end, int n_owner) {
   MatchParams p{};
+  p.n_owner = n_owner;
+  for (int j = 0; j < n_owner; ++j) {
+    p.owner_keys[j] = owner_keys[j];
+    p.owner_end[j] = owner_end[j];
+  }
   p.n_inst = static_cast<int32_t>(n_inst);
   p.n_dests = n_dests;  // cross-GPU: packed atomicMax into every rank's result buffer
   for (int j = 0; j < n_dests; ++j) p.dests[j] = reinterpret_cast<unsigned long long*>(dests[j]);
@@ -1157,8 +1174,9 @@ struct kvx_xmatch {
   uint8_t uuid[16] = {};
   int64_t* peer_keys[KVX_MAX_PEERS] = {};
   uint64_t key_epoch = 0;
-  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // share_keys pushes; fused stage 1's side work
   cudaEvent_t copy_dep = nullptr;
+  cudaEvent_t side_done = nullptr;  // fused stage 1: the side stream's order + preset
   uint64_t* buf(int b) const { return reinterpret_cast<uint64_t*>(mem) + b * max_req; }
   uint64_t* flags() const { return reinterpret_cast<uint64_t*>(mem) + 2 * max_req; }
   uint64_t* keyflags() const { return flags() + KVX_MAX_PEERS; }
@@ -1226,6 +1244,7 @@ int kvx_xmatch_destroy(kvx_xmatch* x) {
   }
   if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
   if (x->copy_dep) cudaEventDestroy(x->copy_dep);
+  if (x->side_done) cudaEventDestroy(x->side_done);
   if (x->keys) cudaFree(x->keys);
   if (x->order) cudaFree(x->order);
   if (x->claim) cudaFree(x->claim);
@@ -1297,6 +1316,7 @@ int kvx_xmatch_key_buffer(kvx_xmatch* x, int64_t max_keys, int64_t** d_keys) {
   KVX_CUDA(cudaMalloc(reinterpret_cast<void**>(&x->keys), 2 * sizeof(int64_t) * max_keys));
   KVX_CUDA(cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking));
   KVX_CUDA(cudaEventCreateWithFlags(&x->copy_dep, cudaEventDisableTiming));
+  KVX_CUDA(cudaEventCreateWithFlags(&x->side_done, cudaEventDisableTiming));
   x->max_keys = max_keys;
   x->peer_keys[x->rank] = x->keys;
   *d_keys = x->keys;
@@ -1383,18 +1403,22 @@ static int xmatch_finish(kvx_xmatch* x, uint64_t e, int64_t n_req, int64_t* d_be
 }
 
 
-// Request-sharded stage 1 with the exchange inside the kernels (see kvx.h).
-// Per step e (parity par = e & 1 selects the key-buffer half):
-//   wait ready(e) from every peer      (their half `par` is preset to -1)
-//   hash this rank's shard -> keys into the local half AND every peer's half
-//   follow: match the WHOLE batch against the local instances as keys land
-//           (local or NVLink-stored), packed atomicMax into every rank's result
-//   signal done(e) to every peer        (my stores into their half `par` ended)
+// Request-sharded stage 1 with the key exchange inside the match kernel (see
+// kvx.h).  Per step e (parity par = e & 1 selects the key-buffer half):
+//   wait ready(e) from every peer   (its half `par` is preset to -1)
+//   hash this rank's shard into the local half `par`
+//   follow: match the WHOLE batch against the local instances beside the
+//           hash, reading each request's keys where its shard's GPU stores
+//           them (local, or NVLink loads of the peer's half) as they appear;
+//           packed atomicMax into every rank's result buffer
+//   signal done(e) to every peer    (my reads of their half `par` ended)
 //   announce / wait / unpack the results (xmatch_finish)
-//   wait done(e - 1) from every peer, preset half par ^ 1, signal ready(e + 1)
-// Every wait is a stream memop; nothing blocks the host.
+//   wait done(e - 1) from every peer, preset my half par ^ 1, signal ready(e + 1)
+// Every wait is a stream memop; nothing blocks the host.  (Pushing each key
+// into the peers' buffers from the hash kernel instead measured 407 us per
+// Config 4 step on 2 GPUs: the remote stores stall the key-folding lane.)
 int kvx_xmatch_hash_match(kvx_xmatch* x, const int32_t* d_tokens, const int64_t* d_tok_off,
-                          int64_t r0, int64_t r1, int64_t bs, const int64_t* d_key_off,
+                          const int64_t* shard_bounds, int64_t bs, const int64_t* d_key_off,
                           int64_t n_req, const kvx_index* const* idx, const int32_t* inst_ids,
                           int64_t n_inst, int64_t* d_best_len, int32_t* d_best_id,
                           int64_t** d_keys_out, void* stream) {
@@ -1403,7 +1427,10 @@ int kvx_xmatch_hash_match(kvx_xmatch* x, const int32_t* d_tokens, const int64_t*
   KVX_REQUIRE(n_inst <= KVX_MAX_INSTANCES, "kvx_xmatch_hash_match: too many instances");
   KVX_REQUIRE(idx != nullptr && inst_ids != nullptr, "kvx_xmatch_hash_match: NULL instances");
   KVX_REQUIRE(n_req >= 1 && n_req <= x->max_req, "kvx_xmatch_hash_match: n_req out of range");
-  KVX_REQUIRE(0 <= r0 && r0 <= r1 && r1 <= n_req, "kvx_xmatch_hash_match: bad shard");
+  KVX_REQUIRE(shard_bounds != nullptr && shard_bounds[0] == 0 && shard_bounds[x->world] == n_req,
+              "kvx_xmatch_hash_match: shard bounds must run from 0 to n_req");
+  for (int j = 0; j < x->world; ++j)
+    KVX_REQUIRE(shard_bounds[j] <= shard_bounds[j + 1], "kvx_xmatch_hash_match: bad shard bounds");
   KVX_REQUIRE(d_tokens && d_tok_off && d_key_off && d_best_len && d_best_id,
               "kvx_xmatch_hash_match: NULL array");
   KVX_REQUIRE(bs >= 16 && bs % 16 == 0 && (reinterpret_cast<uintptr_t>(d_tokens) & 15) == 0,
@@ -1423,10 +1450,10 @@ int kvx_xmatch_hash_match(kvx_xmatch* x, const int32_t* d_tokens, const int64_t*
   const uint64_t e = ++x->fused_epoch;
   const int par = static_cast<int>(e & 1);
   int64_t* mine = x->keys + par * x->max_keys;
-  int rc = KVX_OK;
   // a half is preset whole (all bytes 0xff: every key -1), so the next step
   // may be a batch of any size
   const size_t half_bytes = sizeof(int64_t) * static_cast<size_t>(x->max_keys);
+  int rc = KVX_OK;
   if (e == 1) {  // the first step's half: preset and announce
     KVX_CUDA(cudaMemsetAsync(mine, 0xff, half_bytes, s));
     for (int j = 0; j < x->world; ++j) {
@@ -1434,54 +1461,65 @@ int kvx_xmatch_hash_match(kvx_xmatch* x, const int32_t* d_tokens, const int64_t*
       rc = kvx_signal_write(stream, x->peer_flags[j] + 2 * KVX_MAX_PEERS + x->rank, e);
       if (rc) return rc;
     }
+  } else {  // this step's half was preset by the previous step's side work
+    KVX_CUDA(cudaStreamWaitEvent(s, x->side_done, 0));
   }
+  // Side stream, beside this step's hash: the whole-batch order for the
+  // follower, then the NEXT step's half -- once every peer has finished
+  // reading it (step e - 1) -- preset and announced.
+  KVX_CUDA(cudaEventRecord(x->copy_dep, s));
+  KVX_CUDA(cudaStreamWaitEvent(x->copy_stream, x->copy_dep, 0));
+  // whole-batch longest-first order for the follower (also zeroes its claim counter)
+  rc = order_by_length(d_key_off, n_req, x->order, x->claim, x->copy_stream);
+  if (rc) return rc;
+  KVX_CUDA(cudaEventRecord(x->copy_dep, x->copy_stream));
+  for (int j = 0; j < x->world; ++j) {
+    if (j == x->rank) continue;
+    rc = kvx_signal_wait(x->copy_stream, x->doneflags() + j, e - 1);
+    if (rc) return rc;
+  }
+  KVX_CUDA(cudaMemsetAsync(x->keys + (par ^ 1) * x->max_keys, 0xff, half_bytes, x->copy_stream));
+  for (int j = 0; j < x->world; ++j) {
+    if (j == x->rank) continue;
+    rc = kvx_signal_write(x->copy_stream, x->peer_flags[j] + 2 * KVX_MAX_PEERS + x->rank, e + 1);
+    if (rc) return rc;
+  }
+  KVX_CUDA(cudaEventRecord(x->side_done, x->copy_stream));
   for (int j = 0; j < x->world; ++j) {  // every peer's half `par` is preset
     if (j == x->rank) continue;
     rc = kvx_signal_wait(stream, x->readyflags() + j, e);
     if (rc) return rc;
   }
-  // whole-batch longest-first order for the follower (also zeroes its claim counter)
-  rc = order_by_length(d_key_off, n_req, x->order, x->claim, s);
-  if (rc) return rc;
-  int64_t* peers[KVX_MAX_PEERS];
-  int n_peer = 0;
-  for (int k = 1; k < x->world; ++k) {  // start with the next rank: spread the stores
-    const int j = (x->rank + k) % x->world;
-    peers[n_peer++] = x->peer_keys[j] + par * x->max_keys;
-  }
+  KVX_CUDA(cudaStreamWaitEvent(s, x->copy_dep, 0));  // the order
+  const int64_t r0 = shard_bounds[x->rank], r1 = shard_bounds[x->rank + 1];
   if (r1 > r0) {
     bool published = false;
-    rc = hash_publish_launch(d_tokens, d_tok_off + r0, r1 - r0, bs, d_key_off + r0, mine, peers,
-                             n_peer, stream, &published);
+    rc = hash_publish_launch(d_tokens, d_tok_off + r0, r1 - r0, bs, d_key_off + r0, mine, stream,
+                             &published);
     if (rc) return rc;
     KVX_REQUIRE(published, "kvx_xmatch_hash_match: the publishing hash kernel did not run");
   }
   const uint64_t me = ++x->epoch;  // the result exchange's own step counter
   const int b = static_cast<int>(me & 1);
   uint64_t* dests[KVX_MAX_PEERS];
-  for (int j = 0; j < x->world; ++j) dests[j] = x->peer_buf[j][b];
+  const int64_t* owners[KVX_MAX_PEERS];
+  int64_t owner_end[KVX_MAX_PEERS];
+  for (int j = 0; j < x->world; ++j) {
+    dests[j] = x->peer_buf[j][b];
+    owners[j] = x->peer_keys[j] + par * x->max_keys;  // peer_keys[rank] is the local buffer
+    owner_end[j] = shard_bounds[j + 1];
+  }
   rc = match_follow_launch(idx, inst_ids, n_inst, mine, d_key_off, n_req, nullptr, nullptr,
-                           nullptr, x->order, x->claim, stream, dests, x->world);
+                           nullptr, x->order, x->claim, stream, dests, x->world, owners,
+                           owner_end, x->world);
   if (rc) return rc;
-  for (int j = 0; j < x->world; ++j) {  // my stores into every peer's half `par` are done
+  for (int j = 0; j < x->world; ++j) {  // my reads of every peer's half `par` are done
     if (j == x->rank) continue;
     rc = kvx_signal_write(stream, x->peer_flags[j] + 3 * KVX_MAX_PEERS + x->rank, e);
     if (rc) return rc;
   }
   rc = xmatch_finish(x, me, n_req, d_best_len, d_best_id, s);
   if (rc) return rc;
-  // next step's half: every peer finished storing into it (step e - 1), then preset
-  for (int j = 0; j < x->world; ++j) {
-    if (j == x->rank) continue;
-    rc = kvx_signal_wait(stream, x->doneflags() + j, e - 1);
-    if (rc) return rc;
-  }
-  KVX_CUDA(cudaMemsetAsync(x->keys + (par ^ 1) * x->max_keys, 0xff, half_bytes, s));
-  for (int j = 0; j < x->world; ++j) {
-    if (j == x->rank) continue;
-    rc = kvx_signal_write(stream, x->peer_flags[j] + 2 * KVX_MAX_PEERS + x->rank, e + 1);
-    if (rc) return rc;
-  }
   if (d_keys_out) *d_keys_out = mine;
   return KVX_OK;
 }

@@ -95,7 +95,7 @@ _sig("kvx_hash_match_batch", C.c_int, _vp, _vp, _i64, _i64, _vp, _vp, C.POINTER(
 _sig("kvx_hash_match_check", C.c_int, _vp)
 _sig("kvx_xmatch_key_buffer", C.c_int, _vp, _i64, C.POINTER(_vp))
 _sig("kvx_xmatch_share_keys", C.c_int, _vp, _i64, _i64, _vp)
-_sig("kvx_xmatch_hash_match", C.c_int, _vp, _vp, _vp, _i64, _i64, _i64, _vp, _i64,
+_sig("kvx_xmatch_hash_match", C.c_int, _vp, _vp, _vp, C.POINTER(_i64), _i64, _vp, _i64,
      C.POINTER(_vp), C.POINTER(_i32), _i64, _vp, _vp, C.POINTER(_vp), _vp)
 _sig("kvx_index_create", C.c_int, C.c_int, _i64, C.POINTER(_vp))
 _sig("kvx_index_destroy", C.c_int, _vp)
@@ -440,21 +440,23 @@ class XMatch:
         engine over NVLink); `stream` then waits for every peer's shard."""
         check(_L.kvx_xmatch_share_keys(self.h, key_lo, key_hi, _stream(stream)))
 
-    def hash_match(self, tokens: torch.Tensor, tok_off: torch.Tensor, r0: int, r1: int, bs: int,
-                   key_off: torch.Tensor, indices: Sequence[BlockIndex], inst_ids: Sequence[int],
-                   out=None, stream=None):
-        """Request-sharded stage 1 with the exchange inside the kernels: this
-        rank hashes requests [r0, r1) of the batch and stores every key into
-        every rank's key buffer as it is produced; each rank's match kernel
-        follows the keys of the WHOLE batch against its instances and MAXes
-        the result into every rank's buffer.  Collective, once per step.
+    def hash_match(self, tokens: torch.Tensor, tok_off: torch.Tensor, bounds: Sequence[int],
+                   bs: int, key_off: torch.Tensor, indices: Sequence[BlockIndex],
+                   inst_ids: Sequence[int], out=None, stream=None):
+        """Request-sharded stage 1 with the key exchange inside the match
+        kernel: rank k hashes requests [bounds[k], bounds[k+1]) of the batch
+        into its own key buffer; every rank's match kernel follows the keys
+        of the WHOLE batch where they are produced (NVLink loads of the
+        owner's buffer) against its instances and MAXes the result into every
+        rank's buffer.  Collective, once per step, same bounds on every rank.
         Needs key_buffer() sized for the batch, bs % 16 == 0 and one GPU per
-        rank.  Returns (best_len, best_id, keys) -- keys: this step's batch
-        keys on this rank (valid until the step after next)."""
+        rank.  Returns (best_len, best_id, keys) -- keys: this rank's buffer
+        of the step (its own shard's keys valid; until the step after next)."""
         n_inst = len(indices)
         n_req = len(key_off) - 1
         arr = (_vp * max(n_inst, 1))(*[i.h for i in indices])
         ids = (_i32 * max(n_inst, 1))(*[int(i) for i in inst_ids])
+        b = (_i64 * len(bounds))(*[int(v) for v in bounds])
         if out is None:
             out = (torch.empty(n_req, dtype=torch.int64, device=key_off.device),
                    torch.empty(n_req, dtype=torch.int32, device=key_off.device))
@@ -463,9 +465,9 @@ class XMatch:
         if n_keys > getattr(self, "max_keys", 0):
             raise ValidationError("XMatch.hash_match: the batch has more keys than key_buffer()")
         kp = _vp()
-        check(_L.kvx_xmatch_hash_match(self.h, _ptr(tokens), _ptr(tok_off), r0, r1, bs,
-                                       _ptr(key_off), n_req, arr, ids, n_inst, _ptr(best_len),
-                                       _ptr(best_id), C.byref(kp), _stream(stream)))
+        check(_L.kvx_xmatch_hash_match(self.h, _ptr(tokens), _ptr(tok_off), b, bs, _ptr(key_off),
+                                       n_req, arr, ids, n_inst, _ptr(best_len), _ptr(best_id),
+                                       C.byref(kp), _stream(stream)))
         keys = (_wrap_device_bytes(int(kp.value), 8 * n_keys, self.device).view(torch.int64)
                 if kp.value and n_keys else None)
         return best_len, best_id, keys

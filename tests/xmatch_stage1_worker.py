@@ -1,8 +1,8 @@
 """torchrun worker for tests/test_gpu_xmatch.py: request-sharded stage 1 with
-the exchange inside the kernels (kvx_xmatch_hash_match).  Each rank hashes
-its shard of the batch, its hash kernel stores every key into every rank's
-key buffer, and each rank's match kernel follows the whole batch against the
-rank's ONE prefill instance.  Must equal chain_hash_batch over the whole batch
+the key exchange inside the match kernel (kvx_xmatch_hash_match).  Each rank
+hashes its shard of the batch into its own key buffer, and each rank's match
+kernel follows the whole batch (peer shards through NVLink loads) against
+the rank's ONE prefill instance.  Must equal chain_hash_batch over the whole batch
 and find_best_prefix_match over all instances on one GPU, over several steps
 and two batch shapes (exercises both key-buffer halves and the flags).
 KVX_SHARE_GPU=1 (ranks sharing cuda:0): the call must refuse (KVX_EINVAL)."""
@@ -58,8 +58,8 @@ for toks, toff, off_np in batches:
 
     everyone = [index_of(j) for j in range(world)]
     _, ref_len, ref_id = pkg.match_prefix_batch(everyone, ids, keys_ref, koff, want_lens=False)
-    r0, r1 = rank * n_req // world, (rank + 1) * n_req // world
-    plans.append((toks, toff, koff, keys_ref, ref_len, ref_id, everyone[rank], r0, r1))
+    bounds = [j * n_req // world for j in range(world)] + [n_req]
+    plans.append((toks, toff, koff, keys_ref, ref_len, ref_id, everyone[rank], bounds))
     max_keys = max(max_keys, int(koff_np[-1]))
 
 xm = pkg.kvx.XMatch(dev, rank, world, max_req=400)
@@ -71,21 +71,21 @@ for b in blobs:
 torch.cuda.synchronize()
 s = torch.cuda.current_stream()
 if share:
-    toks, toff, koff, *_rest, mine, r0, r1 = plans[0]
+    toks, toff, koff, *_rest, mine, bounds = plans[0]
     try:
-        xm.hash_match(toks, toff, r0, r1, BS, koff, [mine], [ids[rank]], stream=s)
+        xm.hash_match(toks, toff, bounds, BS, koff, [mine], [ids[rank]], stream=s)
         raise SystemExit("shared GPU: kvx_xmatch_hash_match did not refuse")
     except pkg.kvx.ValidationError:
         pass
 else:
     for step, which in enumerate([0, 0, 1, 0, 1, 1, 0]):
-        toks, toff, koff, keys_ref, ref_len, ref_id, mine, r0, r1 = plans[which]
-        best_len, best_id, keys = xm.hash_match(toks, toff, r0, r1, BS, koff, [mine],
+        toks, toff, koff, keys_ref, ref_len, ref_id, mine, bounds = plans[which]
+        best_len, best_id, keys = xm.hash_match(toks, toff, bounds, BS, koff, [mine],
                                                 [ids[rank]], stream=s)
         torch.cuda.synchronize()
         pkg.kvx.check(pkg.kvx._L.kvx_hash_match_check(None))
-        n_keys = keys_ref.numel()
-        assert torch.equal(keys[:n_keys], keys_ref), ("keys", step)
+        k0, k1 = int(koff[bounds[rank]].item()), int(koff[bounds[rank + 1]].item())
+        assert torch.equal(keys[k0:k1], keys_ref[k0:k1]), ("keys", step)
         assert torch.equal(best_len, ref_len), ("best_len", step)
         assert torch.equal(best_id, ref_id), ("best_id", step)
 dist.barrier()
