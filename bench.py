@@ -1174,13 +1174,21 @@ def bench_match_sharded(args, dev, rank, world, s, o):
             _, _, fkeys = step_fused()
         e1.record(s)
         s.synchronize()
-        ms_fused = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
-        pkg.kvx.check(pkg.kvx._L.kvx_hash_match_check(pkg.kvx._stream(s)))
-        ok = (np.array_equal(fkeys.cpu().numpy()[k0:k1], k_ref[k0:k1])  # this GPU's shard
-              and np.array_equal(best_len.cpu().numpy(), want_len)
-              and np.array_equal(best_id.cpu().numpy(), want_id))
-        if not ok:
-            raise SystemExit("FUSED SHARDED STAGE-1 PARITY FAILURE (keys or best match)")
+        ms_f = max_over_ranks(e0.elapsed_time(e1), d) / args.steps
+        try:
+            pkg.kvx.check(pkg.kvx._L.kvx_hash_match_check(pkg.kvx._stream(s)))
+            ok = (np.array_equal(fkeys.cpu().numpy()[k0:k1], k_ref[k0:k1])  # this GPU's shard
+                  and np.array_equal(best_len.cpu().numpy(), want_len)
+                  and np.array_equal(best_id.cpu().numpy(), want_id))
+        except pkg.kvx.KvxError as exc:
+            ok, fused_note = False, str(exc)
+        # every rank must agree (a parity failure on one rank voids the number everywhere)
+        all_ok = max_over_ranks(0.0 if ok else 1.0, d) < 0.5  # no rank failed
+        if all_ok:
+            ms_fused = ms_f
+        else:  # reported, not used: the separate step stays the value
+            fused_note = fused_note or "FUSED SHARDED STAGE-1 PARITY FAILURE (keys or best match)"
+            print(f"[bench] {fused_note}", file=sys.stderr)
     ms = ms_fused if ms_fused is not None else ms_sep
     out = {"value": B.n_blocks / (ms / 1e3), "unit": "blocks/s", "ms_per_step": ms,
            "scaling": "strong",
