@@ -26,23 +26,27 @@ else:
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
 d = f"cuda:{dev}"
 rng = np.random.default_rng(11)  # same inputs on every rank
-BS = 16
 
 
 def batch(n_req, max_tok, misalign):
     lens = rng.integers(0, max_tok, n_req)
-    lens[3] = 0
+    if n_req > 3:
+        lens[3] = 0
     off = (np.concatenate([[0], np.cumsum(lens)]) + misalign).astype(np.int64)
     toks = rng.integers(0, 32000, int(off[-1]) + 8).astype(np.int32)
     return torch.as_tensor(toks, device=d), torch.as_tensor(off, device=d), off
 
 
-batches = [batch(300, 6000, 3), batch(180, 2000, 0)]
+# a large batch, a small one, and one whose single request leaves every
+# other rank's shard empty
+# (and one at block size 32)
+batches = [batch(300, 6000, 3) + (16,), batch(180, 2000, 0) + (16,), batch(1, 9000, 1) + (16,),
+           batch(120, 8000, 2) + (32,)]
 ids = [world - j + 5 for j in range(world)]
 plans = []
 max_keys = 0
-for toks, toff, off_np in batches:
-    keys_ref, koff = pkg.chain_hash_batch(toks, toff, BS)
+for toks, toff, off_np, bs in batches:
+    keys_ref, koff = pkg.chain_hash_batch(toks, toff, bs)
     n_req = len(off_np) - 1
     koff_np = koff.cpu().numpy()
     lens = np.diff(koff_np)
@@ -59,7 +63,7 @@ for toks, toff, off_np in batches:
     everyone = [index_of(j) for j in range(world)]
     _, ref_len, ref_id = pkg.match_prefix_batch(everyone, ids, keys_ref, koff, want_lens=False)
     bounds = [j * n_req // world for j in range(world)] + [n_req]
-    plans.append((toks, toff, koff, keys_ref, ref_len, ref_id, everyone[rank], bounds))
+    plans.append((toks, toff, koff, keys_ref, ref_len, ref_id, everyone[rank], bounds, bs))
     max_keys = max(max_keys, int(koff_np[-1]))
 
 xm = pkg.kvx.XMatch(dev, rank, world, max_req=400)
@@ -71,16 +75,16 @@ for b in blobs:
 torch.cuda.synchronize()
 s = torch.cuda.current_stream()
 if share:
-    toks, toff, koff, *_rest, mine, bounds = plans[0]
+    toks, toff, koff, *_rest, mine, bounds, bs = plans[0]
     try:
-        xm.hash_match(toks, toff, bounds, BS, koff, [mine], [ids[rank]], stream=s)
+        xm.hash_match(toks, toff, bounds, bs, koff, [mine], [ids[rank]], stream=s)
         raise SystemExit("shared GPU: kvx_xmatch_hash_match did not refuse")
     except pkg.kvx.ValidationError:
         pass
 else:
-    for step, which in enumerate([0, 0, 1, 0, 1, 1, 0]):
-        toks, toff, koff, keys_ref, ref_len, ref_id, mine, bounds = plans[which]
-        best_len, best_id, keys = xm.hash_match(toks, toff, bounds, BS, koff, [mine],
+    for step, which in enumerate([0, 0, 1, 0, 2, 1, 3, 1, 0, 2, 3]):
+        toks, toff, koff, keys_ref, ref_len, ref_id, mine, bounds, bs = plans[which]
+        best_len, best_id, keys = xm.hash_match(toks, toff, bounds, bs, koff, [mine],
                                                 [ids[rank]], stream=s)
         torch.cuda.synchronize()
         pkg.kvx.check(pkg.kvx._L.kvx_hash_match_check(None))
