@@ -214,7 +214,9 @@ int kvx_xmatch_share_keys(kvx_xmatch* x, int64_t key_lo, int64_t key_hi, void* s
  * n_req, bs and bounds on every rank.  Needs kvx_xmatch_key_buffer (>= the
  * batch's keys), bs % 16 == 0, 16-byte aligned tokens; KVX_EINVAL if a peer
  * shares this GPU (its kernels would wait on ours).  *d_keys_out (may be
- * NULL): this rank's key buffer of the step (its own shard's keys). */
+ * NULL): this rank's key buffer of the step (its own shard's keys).  Do not
+ * interleave with kvx_xmatch_share_keys on the same exchange (both use the
+ * key buffer's first half). */
 int kvx_xmatch_hash_match(kvx_xmatch* x, const int32_t* d_tokens, const int64_t* d_tok_off,
                           const int64_t* shard_bounds, int64_t bs, const int64_t* d_key_off,
                           int64_t n_req, const kvx_index* const* idx, const int32_t* inst_ids,
