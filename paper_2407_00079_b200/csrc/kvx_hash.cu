@@ -283,7 +283,10 @@ __global__ void __launch_bounds__(kHashThreads, KVX_HASH_MIN_CTAS) block_hash_fu
 // -> L2 -> polling fold lanes on reserved SMs) this removes the content
 // staging traffic, the polling and the reserved SMs.
 namespace hw {
-constexpr int kPrefetch = 3;                    // sub-rounds of tokens in flight
+#ifndef KVX_HASH_PREFETCH
+#define KVX_HASH_PREFETCH 3
+#endif
+constexpr int kPrefetch = KVX_HASH_PREFETCH;  // sub-rounds of tokens in flight
 constexpr int kSlots = kPrefetch + 1;
 constexpr int kContentLanes = 15;
 constexpr int kRowWords = 20;                   // 16 tokens + misalignment, 16-B rows
